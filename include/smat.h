@@ -1,0 +1,189 @@
+/*
+ * smat.h — C ABI of the B200-native structured-operator engine (libsmat.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `linopkit` (a fastmat-style structured-matrix library): the validated
+ * matrix-free forward (A·x) and backward (A^H·y) transforms of batched column
+ * blocks.  The reference reaches its numpy transform kernels through
+ *
+ *   LinearOperator.forward / backward   pkg/src/linopkit/core.py:128-167
+ *   subclass _forward / _backward hooks pkg/src/linopkit/core.py:114-118
+ *   leaves / composites                 pkg/src/linopkit/leaves.py, composites.py
+ *   kernels dft / fwht / get_plan       pkg/src/linopkit/kernels.py:127-190
+ *
+ * Here the whole operator tree is serialised once into an array of
+ * `smat_node`, compiled into an immutable device plan (`smat_plan_build`,
+ * replacing the per-node recursion of composites.py:49-61 and the plan cache
+ * of kernels.py:150-153), and every application is ONE `smat_apply` call that
+ * launches the plan's fused passes on a CUDA stream.  No torch types cross
+ * this boundary: plain pointers, sizes and a `cudaStream_t` passed as void*.
+ *
+ * Layout: x and y are (rows, ncols) C-contiguous blocks — the numpy/torch
+ * default used by the reference (core.py:128-149): element (i, col) at
+ * i*ncols + col.  Columns are independent.
+ *
+ * Ownership: callers own x, y and the workspace; the plan owns every device
+ * parameter (spectra, twiddles, chirps, diagonals, dense factors).  A plan is
+ * immutable after build; `smat_apply` is reentrant across streams when each
+ * stream uses its own workspace (reference threading contract: core.py:5-7).
+ *
+ * Errors: every entry point returns an `smat_status`; the message of the last
+ * failure on the calling thread is available from `smat_last_error()`.  The
+ * Python layer maps the codes to the reference exception classes
+ * (errors.py:4-65) after doing the reference's own validation first.
+ */
+#ifndef SMAT_H_
+#define SMAT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMAT_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SMAT_API __attribute__((visibility("default")))
+#else
+#define SMAT_API
+#endif
+
+typedef enum smat_status {
+  SMAT_OK = 0,
+  SMAT_BAD_SHAPE = 1,    /* DimensionMismatch / ChainMismatch (errors.py:8, 32) */
+  SMAT_NOT_POW2 = 2,     /* NotPowerOfTwo (errors.py:16)                        */
+  SMAT_BAD_DTYPE = 3,    /* TypeError in coerce_array (core.py:66-68)            */
+  SMAT_CUDA_ERROR = 4,   /* a CUDA runtime failure                               */
+  SMAT_BAD_ARG = 5,      /* ValueError                                           */
+  SMAT_UNSUPPORTED = 6,  /* operator/size combination with no device path       */
+  SMAT_OOM = 7           /* device allocation failed                             */
+} smat_status;
+
+typedef enum smat_dtype {
+  SMAT_F32 = 0,
+  SMAT_F64 = 1,
+  SMAT_C64 = 2,
+  SMAT_C128 = 3,
+  SMAT_I32 = 4,
+  SMAT_I64 = 5
+} smat_dtype;
+
+/* Operator kinds.  Leaves: leaves.py:28-322; composites: composites.py:30-398. */
+typedef enum smat_kind {
+  SMAT_IDENTITY = 0,   /* Identity(n)                      leaves.py:68-79   */
+  SMAT_ZERO = 1,       /* Zero(rows, cols)                 leaves.py:52-65   */
+  SMAT_DIAGONAL = 2,   /* Diagonal(d)  (alias Diag)        leaves.py:82-97   */
+  SMAT_DENSE = 3,      /* Dense(entries) (alias Matrix)    leaves.py:28-49   */
+  SMAT_HADAMARD = 4,   /* Hadamard(order)                  leaves.py:181-204 */
+  SMAT_FOURIER = 5,    /* Fourier(n)                       leaves.py:162-178 */
+  SMAT_CIRCULANT = 6,  /* Circulant(c)                     leaves.py:207-234 */
+  SMAT_TOEPLITZ = 7,   /* Toeplitz(first_col, row_rest)    leaves.py:237-290 */
+  SMAT_LOWRANK = 8,    /* LowRank(U, V[, s]) = U diag(s) V^H   (new type)     */
+  SMAT_PRODUCT = 9,    /* Product(*factors)                composites.py:30-67  */
+  SMAT_SUM = 10,       /* Sum(*terms)                      (new type)           */
+  SMAT_KRON = 11,      /* Kron(*factors)                   composites.py:70-121 */
+  SMAT_PARTIAL = 12,   /* Partial(base, rows, cols)        composites.py:239-320*/
+  SMAT_ADJOINT = 13,   /* Adjoint(base)                    core.py:229-253      */
+  SMAT_BLOCKDIAG = 14, /* BlockDiag(*blocks)               composites.py:196-236*/
+  SMAT_BLOCKS = 15,    /* Blocks(grid)                     composites.py:124-193*/
+  SMAT_SCALED = 16     /* scalar * base (Polynomial/Power building block)       */
+} smat_kind;
+
+/* A host-resident parameter array (copied to the device by plan build). */
+typedef struct smat_param {
+  const void* data; /* host pointer, C-contiguous                     */
+  int64_t len;      /* number of elements                             */
+  int32_t dtype;    /* smat_dtype of `data`                           */
+  int32_t _pad;
+} smat_param;
+
+/*
+ * One node of the serialised operator tree.
+ *   kind     smat_kind
+ *   rows/cols operator shape (core.py:96-106)
+ *   children index range [first_child, first_child + n_children) into the
+ *            `children` array passed to smat_plan_build
+ *   iparam   kind-specific integers:
+ *              HADAMARD: iparam[0] = order
+ *              BLOCKS:   iparam[0] = grid rows, iparam[1] = grid cols
+ *              PARTIAL:  iparam[0] = has_rows, iparam[1] = has_cols,
+ *                        iparam[2] = rows unique, iparam[3] = cols unique
+ *              LOWRANK:  iparam[0] = rank r
+ *   dparam   kind-specific scalars (SCALED: dparam[0] + i dparam[1])
+ *   param    kind-specific arrays:
+ *              DIAGONAL: param[0] = d
+ *              DENSE:    param[0] = entries (rows x cols)
+ *              CIRCULANT:param[0] = first column c
+ *              TOEPLITZ: param[0] = first column, param[1] = first row rest
+ *              LOWRANK:  param[0] = U (rows x r), param[1] = V (cols x r),
+ *                        param[2] = s (r) or empty
+ *              PARTIAL:  param[0] = row indices (I64), param[1] = col indices
+ */
+typedef struct smat_node {
+  int32_t kind;
+  int32_t n_children;
+  int32_t first_child;
+  int32_t _pad;
+  int64_t rows;
+  int64_t cols;
+  int64_t iparam[4];
+  double dparam[2];
+  smat_param param[4];
+} smat_node;
+
+typedef struct smat_plan smat_plan;
+
+/* Compile a serialised operator tree into an immutable device plan for the
+ * working dtype `dtype` on CUDA device `device`.  Replaces operator
+ * construction-time precomputation (Circulant spectrum leaves.py:216, Toeplitz
+ * embedding leaves.py:253-261, DftPlan tables kernels.py:68-93) and the
+ * lru-cached plan registry get_plan (kernels.py:150-153). */
+SMAT_API int smat_plan_build(const smat_node* nodes, int32_t n_nodes, const int32_t* children,
+                    int32_t n_children, int32_t root, int32_t dtype, int32_t device,
+                    smat_plan** out);
+
+/* Device workspace (bytes) one smat_apply of `ncols` columns needs. */
+SMAT_API int smat_workspace_bytes(const smat_plan* plan, int32_t direction, int64_t ncols,
+                         size_t* out_bytes);
+
+/* y = A·x (direction 0, forward — core.py:128-149) or y = A^H·x (direction 1,
+ * backward — core.py:151-167) on device buffers; asynchronous on `stream`,
+ * no allocation, CUDA-graph capturable.  x is (cols, ncols) for direction 0
+ * and (rows, ncols) for direction 1, in the plan dtype except that a real
+ * input to a complex plan may be passed with `x_dtype` = the matching real
+ * dtype (it is promoted on load, core.py:145).  y is written in the plan
+ * dtype. */
+SMAT_API int smat_apply(const smat_plan* plan, int32_t direction, const void* x, int32_t x_dtype,
+               void* y, int64_t ncols, void* workspace, size_t workspace_bytes,
+               void* stream);
+
+/* End-to-end application on HOST buffers (the reference's numpy-in/numpy-out
+ * contract, core.py:128-149): pinned or pageable host x, host y.  Columns are
+ * streamed through the device in chunks so that host->device copies, the
+ * device passes and device->host copies overlap on separate streams. */
+SMAT_API int smat_apply_host(const smat_plan* plan, int32_t direction, const void* x_host,
+                    int32_t x_dtype, void* y_host, int64_t ncols, int32_t chunk_cols);
+
+/* Number of kernel launches one smat_apply issues, and a human-readable
+ * description of the compiled passes (diagnostics, bench gpu_launches). */
+SMAT_API int smat_plan_launches(const smat_plan* plan, int32_t direction, int64_t ncols,
+                       int64_t* out_launches);
+SMAT_API int smat_plan_describe(const smat_plan* plan, char* buf, size_t buf_len);
+
+/* Rows/cols/dtype of a compiled plan. */
+SMAT_API int smat_plan_shape(const smat_plan* plan, int64_t* rows, int64_t* cols, int32_t* dtype);
+
+SMAT_API void smat_plan_free(smat_plan* plan);
+
+/* Thread-local message of the last failing call on this thread. */
+SMAT_API const char* smat_last_error(void);
+
+SMAT_API int smat_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMAT_H_ */

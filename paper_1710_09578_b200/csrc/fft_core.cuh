@@ -1,0 +1,199 @@
+// fft_core.cuh — register/shared-memory FFT and FWHT building blocks (sm_100a).
+//
+// Replaces the numpy radix-2 DIT of the reference (DftPlan._pow2,
+// pkg/src/linopkit/kernels.py:95-109: bit-reversal gather + log2 n full-array
+// passes) by a Stockham auto-sort formulation computed in registers: every
+// thread owns E elements of one column, performs radix-R butterflies on them
+// (R in {2,4,8,16}, constant twiddles folded at compile time) and exchanges
+// through shared memory between stages.  No bit-reversal pass exists; input
+// and output are both in natural order, so the first stage loads straight
+// from HBM and the last stage stores straight to HBM.
+//
+// The FWHT (kernels.py:164-190) uses the same thread/element geometry without
+// twiddles and keeps the reference's stage order (stride 1, 2, 4, ... — stride-1
+// first, kernels.py:181-189), which makes fp64 results bit-identical to the
+// reference and integer results exact.
+#pragma once
+
+#include "common.cuh"
+
+namespace smat {
+
+// ------------------------------------------------------ stage bookkeeping --
+// A length-N transform with E elements per thread runs stages of radix E
+// (forward list: E, E, ..., rem) or the mirrored list (rem, E, ..., E).
+__host__ __device__ constexpr int st_count(int N, int E) {
+  int s = 0, m = 1;
+  while (m < N) {
+    m *= (N / m >= E ? E : N / m);
+    ++s;
+  }
+  return s;
+}
+__host__ __device__ constexpr int st_radix_fwd(int N, int E, int s) {
+  int m = 1, r = 1;
+  for (int i = 0; i <= s; ++i) {
+    r = (N / m >= E ? E : N / m);
+    m *= r;
+  }
+  return r;
+}
+__host__ __device__ constexpr int st_radix(int N, int E, int s, bool mirror) {
+  return mirror ? st_radix_fwd(N, E, st_count(N, E) - 1 - s) : st_radix_fwd(N, E, s);
+}
+__host__ __device__ constexpr int st_ns(int N, int E, int s, bool mirror) {
+  int m = 1;
+  for (int i = 0; i < s; ++i) m *= st_radix(N, E, i, mirror);
+  return m;
+}
+
+// ----------------------------------------------------- constant twiddles ---
+// d * W_16^t, W_16 = exp(-2*pi*i/16), t in [0, 8) known at compile time.
+template <class C>
+__device__ __forceinline__ C mul_w16(C d, const int t) {
+  using R = typename RealOf<C>::T;
+  const R c1 = R(0.92387953251128675613), s1 = R(0.38268343236508977173),
+          h = R(0.70710678118654752440);
+  switch (t) {
+    case 0: return d;
+    case 1: return mk(d.x * c1 + d.y * s1, d.y * c1 - d.x * s1);
+    case 2: return mk((d.x + d.y) * h, (d.y - d.x) * h);
+    case 3: return mk(d.x * s1 + d.y * c1, d.y * s1 - d.x * c1);
+    case 4: return mk(d.y, -d.x);
+    case 5: return mk(d.y * c1 - d.x * s1, -(d.x * c1 + d.y * s1));
+    case 6: return mk((d.y - d.x) * h, -(d.x + d.y) * h);
+    default: return mk(d.y * s1 - d.x * c1, -(d.x * s1 + d.y * c1));
+  }
+}
+
+__host__ __device__ constexpr int bitrev_c(int v, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+__host__ __device__ constexpr int log2_c(int n) { return n <= 1 ? 0 : 1 + log2_c(n / 2); }
+
+// In-register forward DFT of R = 2..16 points, natural order in and out.
+template <int R, class C>
+__device__ __forceinline__ void dft_small(C* a) {
+  if constexpr (R == 1) {
+    return;
+  } else {
+#pragma unroll
+    for (int half = R / 2; half >= 1; half >>= 1) {
+#pragma unroll
+      for (int blk = 0; blk < R; blk += 2 * half) {
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+          C x = a[blk + q], y = a[blk + q + half];
+          a[blk + q] = x + y;
+          a[blk + q + half] = mul_w16(x - y, q * (16 / (2 * half)));
+        }
+      }
+    }
+    C t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) t[i] = a[bitrev_c(i, log2_c(R))];
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = t[i];
+  }
+}
+
+// In-register Walsh-Hadamard of R points, stride-1-first (kernels.py:181-189).
+template <int R, class T>
+__device__ __forceinline__ void wht_small(T* a) {
+#pragma unroll
+  for (int h = 1; h < R; h <<= 1) {
+#pragma unroll
+    for (int blk = 0; blk < R; blk += 2 * h) {
+#pragma unroll
+      for (int q = 0; q < h; ++q) {
+        T x = a[blk + q], y = a[blk + q + h];
+        a[blk + q] = x + y;
+        a[blk + q + h] = x - y;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------- block FFT (Stockham) ----
+// Thread (j, cs) of a tile holds, at stage s (radix R, stride NS), the inputs
+// of butterflies bb = j + u*TPC (u < E/R): elements bb + r*N/R.  Outputs go to
+// (bb/NS)*NS*R + bb%NS + r*NS.  `sm` is the tile's shared buffer, element
+// (idx, cs) at sm[idx*CT + cs].  `tw` is W_4096^t (t < 4096).
+template <class C, int N, int E, int CT, bool MIR, int S>
+__device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* __restrict__ tw) {
+  constexpr int NST = st_count(N, E);
+  if constexpr (S < NST) {
+    constexpr int R = st_radix(N, E, S, MIR);
+    constexpr int NS = st_ns(N, E, S, MIR);
+    constexpr int TPC = N / E;
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+      if constexpr (NS > 1) {
+        const int bb = j + u * TPC;
+        const int k = bb & (NS - 1);
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+          a[u * R + r] = cmul(a[u * R + r], __ldg(&tw[(r * k) * (4096 / (NS * R))]));
+      }
+      dft_small<R>(a + u * R);
+    }
+    if constexpr (S + 1 < NST) {
+      constexpr int R2 = st_radix(N, E, S + 1, MIR);
+      __syncthreads();  // previous readers of sm are done
+#pragma unroll
+      for (int u = 0; u < E / R; ++u) {
+        const int bb = j + u * TPC;
+        const int k = bb & (NS - 1);
+        const int base = (bb - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[(base + r * NS) * CT + cs] = a[u * R + r];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < E / R2; ++u) {
+        const int bb = j + u * TPC;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[(bb + r * (N / R2)) * CT + cs];
+      }
+      fft_stages<C, N, E, CT, MIR, S + 1>(a, sm, j, cs, tw);
+    }
+  }
+}
+
+// Generic in-tile FWHT: group g handles strides S_g..S_g*R/2 in registers.
+template <class T, int N, int E, int CT, int S>
+__device__ __forceinline__ void wht_stages(T* a, T* sm, int j, int cs) {
+  constexpr int NST = st_count(N, E);
+  if constexpr (S < NST) {
+    constexpr int R = st_radix(N, E, S, false);
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) wht_small<R>(a + u * R);
+    if constexpr (S + 1 < NST) {
+      constexpr int NS = st_ns(N, E, S, false);
+      constexpr int R2 = st_radix(N, E, S + 1, false);
+      constexpr int NS2 = st_ns(N, E, S + 1, false);
+      constexpr int TPC = N / E;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < E / R; ++u) {
+        const int bb = j + u * TPC;
+        const int base = (bb / NS) * (NS * R) + (bb % NS);
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[(base + r * NS) * CT + cs] = a[u * R + r];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < E / R2; ++u) {
+        const int bb = j + u * TPC;
+        const int base = (bb / NS2) * (NS2 * R2) + (bb % NS2);
+#pragma unroll
+        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[(base + r * NS2) * CT + cs];
+      }
+      wht_stages<T, N, E, CT, S + 1>(a, sm, j, cs);
+    }
+  }
+}
+
+}  // namespace smat

@@ -1,0 +1,1103 @@
+// plan.cu — plan compiler and generic interpreter of the structured-operator tree.
+//
+// Leaves map onto tiled FFT / FWHT passes (tile_kernels.cu) and pointwise /
+// GEMM passes (misc_kernels.cu); composites orchestrate them over strided views
+// so that no composite ever materialises a reshaped or transposed copy (the
+// reference's Kron._pair_apply loops over columns with reshape/transpose
+// copies, composites.py:96-107; here a Kronecker mode is just a stride).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+#include "plan.cuh"
+
+namespace smat {
+
+// ============================================================ helpers =====
+static int cplx_of(int dt) { return dt_complex_of(dt); }
+
+DevBuf* new_buf(Plan& p, int dt, int64_t len) {
+  auto b = std::make_unique<DevBuf>();
+  b->dt = dt;
+  b->len = len;
+  b->bytes = size_t(len) * dt_size(dt);
+  if (b->bytes) {
+    cudaError_t e = cudaMalloc(&b->p, b->bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(SMAT_OOM, "plan parameter allocation of " + std::to_string(b->bytes) + " bytes failed");
+    }
+  }
+  DevBuf* r = b.get();
+  p.bufs.push_back(std::move(b));
+  return r;
+}
+
+// Host conversion of a parameter array into `target` element type.
+static std::vector<unsigned char> convert_host(const smat_param& prm, int target) {
+  const int64_t n = prm.len;
+  std::vector<unsigned char> out(size_t(n) * dt_size(target));
+  auto get = [&](int64_t i, double& re, double& im) {
+    re = im = 0;
+    switch (prm.dtype) {
+      case SMAT_F32: re = ((const float*)prm.data)[i]; break;
+      case SMAT_F64: re = ((const double*)prm.data)[i]; break;
+      case SMAT_C64: re = ((const float*)prm.data)[2 * i]; im = ((const float*)prm.data)[2 * i + 1]; break;
+      case SMAT_C128: re = ((const double*)prm.data)[2 * i]; im = ((const double*)prm.data)[2 * i + 1]; break;
+      case SMAT_I32: re = double(((const int32_t*)prm.data)[i]); break;
+      case SMAT_I64: re = double(((const int64_t*)prm.data)[i]); break;
+      default: throw Error(SMAT_BAD_DTYPE, "parameter dtype");
+    }
+  };
+  if (dt_int(target)) {
+    SMAT_CHECK(dt_int(prm.dtype), SMAT_BAD_DTYPE, "integer plan needs integer parameters");
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t v = prm.dtype == SMAT_I32 ? ((const int32_t*)prm.data)[i] : ((const int64_t*)prm.data)[i];
+      if (target == SMAT_I32) ((int32_t*)out.data())[i] = int32_t(v);
+      else ((int64_t*)out.data())[i] = v;
+    }
+    return out;
+  }
+  SMAT_CHECK(dt_complex(target) || !dt_complex(prm.dtype), SMAT_BAD_DTYPE,
+             "complex parameter in a real plan");
+  for (int64_t i = 0; i < n; ++i) {
+    double re, im;
+    get(i, re, im);
+    switch (target) {
+      case SMAT_F32: ((float*)out.data())[i] = float(re); break;
+      case SMAT_F64: ((double*)out.data())[i] = re; break;
+      case SMAT_C64: ((float*)out.data())[2 * i] = float(re); ((float*)out.data())[2 * i + 1] = float(im); break;
+      case SMAT_C128: ((double*)out.data())[2 * i] = re; ((double*)out.data())[2 * i + 1] = im; break;
+    }
+  }
+  return out;
+}
+
+DevBuf* upload_param(Plan& p, const smat_param& prm, int target_dt) {
+  DevBuf* b = new_buf(p, target_dt, prm.len);
+  if (prm.len) {
+    auto h = convert_host(prm, target_dt);
+    SMAT_CUDA(cudaMemcpy(b->p, h.data(), h.size(), cudaMemcpyHostToDevice));
+  }
+  return b;
+}
+
+// complex128 device array -> plan complex precision (in place copy into new buffer)
+__global__ void c128_to_c64_kernel(const double2* a, float2* b, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    b[i] = make_float2(float(a[i].x), float(a[i].y));
+}
+static DevBuf* narrow_c128(Plan& p, DevBuf* src, int cdt) {
+  if (cdt == SMAT_C128) return src;
+  DevBuf* d = new_buf(p, SMAT_C64, src->len);
+  c128_to_c64_kernel<<<1184, 256>>>((const double2*)src->p, (float2*)d->p, src->len);
+  SMAT_CUDA(cudaGetLastError());
+  return d;
+}
+
+// ------------------------------------------------------ view utilities -----
+// Merge (o1, o2) into a single outer index when both views allow it, so that
+// multi-pass transforms see n1 == 1.  Returns false when not mergeable.
+static bool merge_outer(Geo& g, Blk& x, Blk& y) {
+  if (g.n1 == 1) return true;
+  if (g.n2 == 1) {
+    g.n2 = g.n1;
+    g.n1 = 1;
+    x.s2 = x.s1;
+    y.s2 = y.s1;
+    return true;
+  }
+  if (x.s1 == g.n2 * x.s2 && y.s1 == g.n2 * y.s2) {
+    g.n2 *= g.n1;
+    g.n1 = 1;
+    return true;
+  }
+  return false;
+}
+
+// Host loop over o1 when the outer dims cannot be merged.
+template <class F>
+static void for_each_o1(const Geo& g, const Blk& x, const Blk& y, F f) {
+  Geo g1 = g;
+  g1.n1 = 1;
+  for (int64_t o = 0; o < g.n1; ++o) {
+    Blk xo = x, yo = y;
+    xo.p = (char*)x.p + o * x.s1 * int64_t(dt_size(x.dt));
+    yo.p = (char*)y.p + o * y.s1 * int64_t(dt_size(y.dt));
+    f(g1, xo, yo);
+  }
+}
+
+static void fill_views(FftArgs& a, const Blk& x, const Blk& y, const Geo& g) {
+  a.x = x.p;
+  a.y = y.p;
+  a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
+  a.ys1 = y.s1; a.ys2 = y.s2; a.ysi = y.si;
+  a.n2 = g.n2;
+  a.inner = g.inner;
+  a.nb = g.count();
+  a.x_real = !dt_complex(x.dt);
+  a.y_real = !dt_complex(y.dt);
+}
+
+// Promote a real block into a fresh plan-dtype block.
+static Blk promote(Ctx& c, const Blk& x, const Geo& g, int64_t rows) {
+  if (x.dt == c.dt) return x;
+  Blk t = c.alloc_blk(c.dt, g, rows);
+  PointArgs pa;
+  pa.x = x.p; pa.x_dt = x.dt; pa.y = t.p; pa.y_dt = t.dt;
+  pa.xs1 = x.s1; pa.xs2 = x.s2; pa.xsi = x.si;
+  pa.ys1 = t.s1; pa.ys2 = t.s2; pa.ysi = t.si;
+  pa.n2 = g.n2; pa.inner = g.inner; pa.nb = g.count(); pa.n = rows;
+  c.point(pa);
+  return t;
+}
+
+static void point_copy(Ctx& c, const Blk& x, const Blk& y, const Geo& g, int64_t rows, bool acc,
+                       const void* d = nullptr, bool d_conj = false, bool x_conj = false,
+                       double sre = 1.0, double sim = 0.0) {
+  PointArgs pa;
+  pa.x = x.p; pa.x_dt = x.dt; pa.y = y.p; pa.y_dt = y.dt;
+  pa.xs1 = x.s1; pa.xs2 = x.s2; pa.xsi = x.si;
+  pa.ys1 = y.s1; pa.ys2 = y.s2; pa.ysi = y.si;
+  pa.n2 = g.n2; pa.inner = g.inner; pa.nb = g.count(); pa.n = rows;
+  pa.d = d; pa.d_conj = d_conj; pa.x_conj = x_conj; pa.accumulate = acc;
+  pa.scale_re = sre; pa.scale_im = sim;
+  c.point(pa);
+}
+
+// ================================================= FFT-along-axis engine ====
+// One logical length-Nt transform of every batch of a view, fused with the
+// prologue/epilogue described in FftArgs.  Nt <= 4096 runs as one tile pass;
+// larger powers of two run the four-step decomposition Nt = N1*N2:
+//   pass 1  stride-N1 length-N2 FFTs, twiddle W_Nt^(n1*k2)   x  -> W
+//   pass 2a contiguous length-N1 FFTs written in natural order W -> y
+//   pass 2b (convolution) length-N1 FFT * spectrum, IFFT, twiddle^-1  W -> W
+//   pass 3  (convolution) stride-N1 length-N2 IFFTs               W -> y
+struct XformIO {
+  Blk x;
+  int64_t x_rows = 0;  // rows of x (rows beyond are zero padding)
+  Blk y;
+  int64_t y_rows = 0;  // rows of y to write (truncation)
+  const void* pre = nullptr;
+  bool pre_conj = false;
+  const void* mid = nullptr;  // spectrum -> circular convolution
+  bool mid_conj = false;
+  const void* post = nullptr;
+  bool post_conj = false;
+  bool conj_x = false, conj_y = false, inv = false, acc = false;
+  double scale = 1.0;
+};
+
+static void xform_pass_common(FftArgs& a, Ctx& c) {
+  a.tw = twiddle4096(c.device, cplx_of(c.dt) == SMAT_C128);
+}
+
+static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
+  const int cdt = cplx_of(c.dt);
+  const bool dbl = cdt == SMAT_C128;
+  if (Nt <= kTileMax) {
+    FftArgs a;
+    fill_views(a, io.x, io.y, g);
+    xform_pass_common(a, c);
+    a.n_valid_in = io.x_rows;
+    a.n_valid_out = io.y_rows;
+    a.pre = io.pre; a.pre_conj = io.pre_conj;
+    a.mid = io.mid; a.mid_conj = io.mid_conj;
+    a.post = io.post; a.post_conj = io.post_conj;
+    a.conj_x = io.conj_x; a.conj_y = io.conj_y; a.inv = io.inv && !io.mid;
+    a.scale = io.scale; a.accumulate = io.acc;
+    c.fft(cdt, int(Nt), a);
+    return;
+  }
+  SMAT_CHECK(Nt <= int64_t(kTileMax) * kTileMax, SMAT_UNSUPPORTED,
+             "transform length " + std::to_string(Nt) + " exceeds the two-pass limit 2^24");
+  if (!merge_outer(g, io.x, io.y)) {
+    for_each_o1(g, io.x, io.y, [&](const Geo& g1, const Blk& xo, const Blk& yo) {
+      XformIO io1 = io;
+      io1.x = xo;
+      io1.y = yo;
+      run_xform(c, Nt, g1, io1);
+    });
+    return;
+  }
+  const int64_t ic = g.inner, O = g.n2;
+  SMAT_CHECK(io.x.si == ic && io.y.si == ic, SMAT_UNSUPPORTED, "four-step FFT needs row-contiguous views");
+  const int l = ilog2(Nt);
+  const int64_t N1 = int64_t(1) << ((l + 1) / 2);
+  const int64_t N2 = Nt / N1;
+  const TwPair tw = twiddle_pair(c.device, Nt, dbl);
+  // plain inverse transform = conj(F conj(.)) spread over the passes
+  bool conj_first = io.conj_x, conj_last = io.conj_y;
+  if (io.inv && !io.mid) {
+    conj_first = !conj_first;
+    conj_last = !conj_last;
+  }
+  const size_t m0 = c.mark();
+  Geo gw;
+  gw.n2 = O;
+  gw.inner = ic;
+  Blk W = c.alloc_blk(cdt, gw, Nt);
+  // ---- pass 1: x -> W
+  {
+    FftArgs a;
+    xform_pass_common(a, c);
+    a.x = io.x.p; a.x_real = !dt_complex(io.x.dt);
+    a.xs1 = 0; a.xs2 = io.x.s2; a.xsi = N1 * io.x.si;
+    a.y = W.p; a.y_real = 0;
+    a.ys1 = 0; a.ys2 = W.s2; a.ysi = N1 * ic;
+    a.n2 = O; a.inner = N1 * ic; a.nb = O * N1 * ic;
+    a.g_div = ic; a.g_mod = N1; a.gin_stride = N1;
+    a.n_valid_in = io.x_rows;
+    a.pre = io.pre; a.pre_conj = io.pre_conj; a.conj_x = conj_first;
+    a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+    c.fft(cdt, int(N2), a);
+  }
+  if (!io.mid) {
+    // ---- pass 2 (plain): W -> y in natural order
+    FftArgs a;
+    xform_pass_common(a, c);
+    a.x = W.p; a.x_real = 0;
+    a.xs1 = W.s2; a.xs2 = N1 * ic; a.xsi = ic;
+    a.y = io.y.p; a.y_real = !dt_complex(io.y.dt);
+    a.ys1 = io.y.s2; a.ys2 = io.y.si; a.ysi = N2 * io.y.si;
+    a.n2 = N2; a.inner = ic; a.nb = O * N2 * ic;
+    a.g_div = ic; a.g_mod = N2; a.gout_stride = N2;
+    a.n_valid_out = io.y_rows;
+    a.post = io.post; a.post_conj = io.post_conj; a.conj_y = conj_last;
+    a.scale = io.scale; a.accumulate = io.acc;
+    c.fft(cdt, int(N1), a);
+  } else {
+    // ---- pass 2 (convolution): W -> W
+    {
+      FftArgs a;
+      xform_pass_common(a, c);
+      a.x = W.p; a.y = W.p;
+      a.xs1 = W.s2; a.xs2 = N1 * ic; a.xsi = ic;
+      a.ys1 = W.s2; a.ys2 = N1 * ic; a.ysi = ic;
+      a.n2 = N2; a.inner = ic; a.nb = O * N2 * ic;
+      a.g_div = ic; a.g_mod = N2;
+      a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = N2;
+      a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+      c.fft(cdt, int(N1), a);
+    }
+    // ---- pass 3: W -> y
+    {
+      FftArgs a;
+      xform_pass_common(a, c);
+      a.x = W.p; a.x_real = 0;
+      a.xs1 = 0; a.xs2 = W.s2; a.xsi = N1 * ic;
+      a.y = io.y.p; a.y_real = !dt_complex(io.y.dt);
+      a.ys1 = 0; a.ys2 = io.y.s2; a.ysi = N1 * io.y.si;
+      a.n2 = O; a.inner = N1 * ic; a.nb = O * N1 * ic;
+      a.g_div = ic; a.g_mod = N1; a.gout_stride = N1;
+      a.n_valid_out = io.y_rows;
+      a.inv = 1;
+      a.post = io.post; a.post_conj = io.post_conj; a.conj_y = io.conj_y;
+      a.scale = io.scale; a.accumulate = io.acc;
+      c.fft(cdt, int(N2), a);
+    }
+  }
+  c.release(m0);
+}
+
+// ==================================================== FWHT engine =========
+static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& x, const Blk& y,
+                     bool acc, int64_t x_rows, int64_t y_rows) {
+  WhtArgs a;
+  const int64_t hi_cnt = int64_t(1) << (order - lo - w);
+  a.x = x.p; a.y = y.p;
+  a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
+  a.ys1 = y.s1; a.ys2 = y.s2; a.ysi = y.si;
+  a.n2 = g.n2; a.inner = g.inner; a.nb = g.count();
+  if (lo > 0 || hi_cnt > 1) {
+    // fold: outer1 = O (stride s2), outer2 = high bits, inner = (low bits, c)
+    a.xs1 = x.s2; a.xs2 = (int64_t(1) << (lo + w)) * x.si; a.xsi = (int64_t(1) << lo) * x.si;
+    a.ys1 = y.s2; a.ys2 = (int64_t(1) << (lo + w)) * y.si; a.ysi = (int64_t(1) << lo) * y.si;
+    a.n2 = hi_cnt;
+    a.inner = (int64_t(1) << lo) * g.inner;
+    a.nb = g.n2 * hi_cnt * a.inner;
+    a.g_div = g.inner;
+    a.g_mod = int64_t(1) << lo;
+    a.gin_stride = a.gout_stride = int64_t(1) << lo;
+    // global row = l + 2^lo * (m + 2^w * h): only the l part is in goff; the
+    // validity masks of multi-pass transforms are applied on the full rows, so
+    // they are only allowed on single-pass calls.
+  }
+  a.n_valid_in = x_rows;
+  a.n_valid_out = y_rows;
+  a.accumulate = acc;
+  c.wht(c.dt, 1 << w, a);
+}
+
+static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc) {
+  const int64_t N = int64_t(1) << order;
+  if (N == 1) {
+    point_copy(c, x, y, g, 1, acc);
+    return;
+  }
+  if (N <= kTileMax) {
+    wht_pass(c, order, 0, order, g, x, y, acc, INT64_MAX, INT64_MAX);
+    return;
+  }
+  if (!merge_outer(g, x, y)) {
+    for_each_o1(g, x, y, [&](const Geo& g1, const Blk& xo, const Blk& yo) { run_wht(c, order, g1, xo, yo, acc); });
+    return;
+  }
+  SMAT_CHECK(x.si == g.inner, SMAT_UNSUPPORTED, "multi-pass FWHT needs row-contiguous input");
+  const int npass = (order + 11) / 12;
+  std::vector<int> widths(npass, order / npass);
+  for (int i = 0; i < order % npass; ++i) widths[i] += 1;
+  const size_t m0 = c.mark();
+  Blk T = y;
+  const bool y_ok = !acc && y.si == g.inner;
+  if (!y_ok) T = c.alloc_blk(c.dt, g, N);
+  int lo = 0;
+  for (int p = 0; p < npass; ++p) {
+    const bool last = p == npass - 1;
+    const Blk& src = p == 0 ? x : T;
+    const Blk& dst = (last && !y_ok) ? y : T;
+    wht_pass(c, order, lo, widths[p], g, src, dst, last && !y_ok ? acc : false, INT64_MAX, INT64_MAX);
+    lo += widths[p];
+  }
+  c.release(m0);
+}
+
+// ========================================================== leaf nodes =====
+struct IdentityNode : Node {
+  std::string describe() const override { return "Identity(" + std::to_string(rows) + ")"; }
+  bool accepts_real() const override { return true; }
+  bool is_identity() const override { return true; }
+  void apply(Ctx& c, bool, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    point_copy(c, x, y, g, rows, acc);
+  }
+};
+
+struct ZeroNode : Node {
+  std::string describe() const override { return "Zero"; }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk&, const Blk& y, const Geo& g, bool acc) override {
+    if (acc) return;
+    PointArgs pa;
+    pa.y = y.p; pa.y_dt = y.dt;
+    pa.ys1 = y.s1; pa.ys2 = y.s2; pa.ysi = y.si;
+    pa.n2 = g.n2; pa.inner = g.inner; pa.nb = g.count(); pa.n = adj ? cols : rows;
+    c.point(pa);
+  }
+};
+
+struct DiagNode : Node {
+  DevBuf* d = nullptr;
+  std::string describe() const override { return "Diagonal(" + std::to_string(rows) + ")"; }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    point_copy(c, x, y, g, rows, acc, d->p, adj);
+  }
+};
+
+struct DenseNode : Node {
+  DevBuf* A = nullptr;
+  std::string describe() const override {
+    return "Dense(" + std::to_string(rows) + "x" + std::to_string(cols) + ")";
+  }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, adj ? rows : cols);
+    GemmArgs a;
+    a.A = A->p;
+    a.lda = cols;
+    a.adj = adj;
+    a.m = adj ? cols : rows;
+    a.k = adj ? rows : cols;
+    a.x = x.p; a.y = y.p;
+    a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
+    a.ys1 = y.s1; a.ys2 = y.s2; a.ysi = y.si;
+    a.n1 = g.n1; a.n2 = g.n2; a.inner = g.inner;
+    a.accumulate = acc;
+    c.gemm(a);
+    c.release(m0);
+  }
+};
+
+struct LowRankNode : Node {
+  DevBuf *U = nullptr, *V = nullptr, *s = nullptr;
+  int64_t r = 0;
+  std::string describe() const override { return "LowRank(rank " + std::to_string(r) + ")"; }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    // fwd: y = U diag(s) V^H x ; adj: x' = V diag(conj s) U^H y
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, adj ? rows : cols);
+    DevBuf* first = adj ? U : V;   // contracted with x (conj-transposed)
+    DevBuf* second = adj ? V : U;  // expands back
+    const int64_t kin = adj ? rows : cols, kout = adj ? cols : rows;
+    Blk t = c.alloc_blk(c.dt, g, r);
+    GemmArgs a;
+    a.A = first->p; a.lda = r; a.adj = 1; a.m = r; a.k = kin;
+    a.x = x.p; a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
+    a.y = t.p; a.ys1 = t.s1; a.ys2 = t.s2; a.ysi = t.si;
+    a.n1 = g.n1; a.n2 = g.n2; a.inner = g.inner;
+    if (s) { a.rowscale = s->p; a.rowscale_conj = adj; }
+    c.gemm(a);
+    GemmArgs b;
+    b.A = second->p; b.lda = r; b.adj = 0; b.m = kout; b.k = r;
+    b.x = t.p; b.xs1 = t.s1; b.xs2 = t.s2; b.xsi = t.si;
+    b.y = y.p; b.ys1 = y.s1; b.ys2 = y.s2; b.ysi = y.si;
+    b.n1 = g.n1; b.n2 = g.n2; b.inner = g.inner;
+    b.accumulate = acc;
+    c.gemm(b);
+    c.release(m0);
+  }
+};
+
+struct HadamardNode : Node {
+  int order = 0;
+  std::string describe() const override { return "Hadamard(" + std::to_string(order) + ")"; }
+  void apply(Ctx& c, bool, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, rows);
+    run_wht(c, order, g, x, y, acc);
+    c.release(m0);
+  }
+};
+
+// Fourier(n): forward DFT (kernels.py:156-161, leaves.py:171-172), backward
+// F^H = n * IDFT (leaves.py:174-175); Bluestein for non powers of two
+// (kernels.py:83-93, 111-125).
+struct FourierNode : Node {
+  int64_t n = 0, M = 0;
+  DevBuf* chirp = nullptr;   // plan complex precision, length n
+  DevBuf* kspec = nullptr;   // FFT_M of the Bluestein kernel, length M
+  std::string describe() const override {
+    return "Fourier(" + std::to_string(n) + (M ? ", Bluestein M=" + std::to_string(M) : "") + ")";
+  }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    XformIO io;
+    io.x = x; io.x_rows = n; io.y = y; io.y_rows = n; io.acc = acc;
+    if (!M) {
+      io.inv = adj;  // F^H = unnormalised inverse
+      run_xform(c, n, g, io);
+      return;
+    }
+    io.pre = chirp->p; io.mid = kspec->p; io.post = chirp->p;
+    io.scale = 1.0 / double(M);
+    io.conj_x = adj; io.conj_y = adj;  // F^H y = conj(F conj(y))
+    run_xform(c, M, g, io);
+  }
+};
+
+// Circulant(c) (leaves.py:207-234): IFFT(spec * FFT(x)); backward uses conj(spec).
+struct CirculantNode : Node {
+  int64_t n = 0;
+  DevBuf* spec = nullptr;
+  std::string describe() const override { return "Circulant(" + std::to_string(n) + ")"; }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    XformIO io;
+    io.x = x; io.x_rows = n; io.y = y; io.y_rows = n; io.acc = acc;
+    io.mid = spec->p; io.mid_conj = adj;
+    io.scale = 1.0 / double(n);
+    run_xform(c, n, g, io);
+  }
+};
+
+// Toeplitz(col, row_rest) (leaves.py:237-290): circulant embedding of length L.
+struct ToeplitzNode : Node {
+  int64_t L = 0;
+  DevBuf* spec = nullptr;
+  std::string describe() const override {
+    return "Toeplitz(" + std::to_string(rows) + "x" + std::to_string(cols) + ", L=" + std::to_string(L) + ")";
+  }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    XformIO io;
+    io.x = x; io.x_rows = adj ? rows : cols;
+    io.y = y; io.y_rows = adj ? cols : rows;
+    io.acc = acc;
+    io.mid = spec->p; io.mid_conj = adj;
+    io.scale = 1.0 / double(L);
+    run_xform(c, L, g, io);
+  }
+};
+
+// ===================================================== composite nodes =====
+struct AdjointNode : Node {
+  Node* base = nullptr;
+  std::string describe() const override { return "Adjoint(" + base->describe() + ")"; }
+  bool accepts_real() const override { return base->accepts_real(); }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    base->apply(c, !adj, x, y, g, acc);
+  }
+};
+
+// Product(A, B, C) = A·B·C applied right to left (composites.py:49-61).
+struct ProductNode : Node {
+  std::vector<Node*> f;
+  std::string describe() const override {
+    std::string s = "Product(";
+    for (size_t i = 0; i < f.size(); ++i) s += (i ? ", " : "") + f[i]->describe();
+    return s + ")";
+  }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    std::vector<Node*> seq;  // order of application
+    if (!adj) seq.assign(f.rbegin(), f.rend());
+    else seq.assign(f.begin(), f.end());
+    const size_t m0 = c.mark();
+    Blk cur = x0;
+    if (cur.dt != c.dt && !seq[0]->accepts_real()) cur = promote(c, x0, g, adj ? rows : cols);
+    for (size_t i = 0; i < seq.size(); ++i) {
+      Node* op = seq[i];
+      const int64_t nout = adj ? op->cols : op->rows;
+      if (i + 1 == seq.size()) {
+        op->apply(c, adj, cur, y, g, acc);
+      } else {
+        const size_t mk = c.mark();
+        Blk nxt = c.alloc_blk(c.dt, g, nout);
+        op->apply(c, adj, cur, nxt, g, false);
+        // keep nxt alive; release the previous intermediate only if it sits
+        // below nxt (stack discipline: we simply never release inside the chain)
+        (void)mk;
+        cur = nxt;
+      }
+    }
+    c.release(m0);
+  }
+};
+
+// Sum(*terms): y = sum_k T_k x (new type; the reference expresses it with
+// Blocks([[A, B]])·Blocks([[I], [I]]), composites.py:171-178).
+struct SumNode : Node {
+  std::vector<Node*> t;
+  std::string describe() const override {
+    std::string s = "Sum(";
+    for (size_t i = 0; i < t.size(); ++i) s += (i ? ", " : "") + t[i]->describe();
+    return s + ")";
+  }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk xc = x0;
+    bool need = false;
+    for (Node* op : t) need |= !op->accepts_real();
+    if (x0.dt != c.dt && need) xc = promote(c, x0, g, adj ? rows : cols);
+    for (size_t i = 0; i < t.size(); ++i) {
+      const Blk& xi = t[i]->accepts_real() ? x0 : xc;
+      t[i]->apply(c, adj, xi, y, g, acc || i > 0);
+    }
+    c.release(m0);
+  }
+};
+
+// Kron(A_0, ..., A_{m-1}), np.kron index order (first factor slowest,
+// composites.py:96-107): mode a is a strided batched transform.
+struct KronNode : Node {
+  std::vector<Node*> f;
+  std::string describe() const override {
+    std::string s = "Kron(";
+    for (size_t i = 0; i < f.size(); ++i) s += (i ? ", " : "") + f[i]->describe();
+    return s + ")";
+  }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y0, const Geo& g0, bool acc) override {
+    const size_t m0 = c.mark();
+    Geo g = g0;
+    Blk x = promote(c, x0, g0, adj ? rows : cols);
+    Blk y = y0;
+    const int m = int(f.size());
+    std::vector<int64_t> sz(m);
+    for (int a = 0; a < m; ++a) sz[a] = adj ? f[a]->rows : f[a]->cols;  // current (input) sizes
+    auto total = [&]() {
+      int64_t t = 1;
+      for (int64_t v : sz) t *= v;
+      return t;
+    };
+    if (!merge_outer(g, x, y) || x.si != g.inner || y.si != g.inner) {
+      // make both ends contiguous
+      Blk xc = c.alloc_blk(c.dt, g0, total());
+      point_copy(c, x, xc, g0, total(), false);
+      int64_t outrows = adj ? cols : rows;
+      Blk yc = c.alloc_blk(c.dt, g0, outrows);
+      Geo gc = g0;
+      gc.n2 = g0.n1 * g0.n2;
+      gc.n1 = 1;
+      Blk xcc = xc, ycc = yc;
+      xcc.s2 = total() * g0.inner;
+      ycc.s2 = outrows * g0.inner;
+      apply_modes(c, adj, xcc, ycc, gc, false, sz);
+      point_copy(c, yc, y0, g0, outrows, acc);
+      c.release(m0);
+      return;
+    }
+    apply_modes(c, adj, x, y, g, acc, sz);
+    c.release(m0);
+  }
+
+  void apply_modes(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc,
+                   std::vector<int64_t> sz) {
+    const int m = int(f.size());
+    std::vector<int> order;
+    for (int a = m - 1; a >= 0; --a)
+      if (!f[a]->is_identity()) order.push_back(a);
+    const int64_t O = g.n2, ic = g.inner;
+    if (order.empty()) {
+      int64_t t = 1;
+      for (int64_t v : sz) t *= v;
+      point_copy(c, x, y, g, t, acc);
+      return;
+    }
+    Blk cur = x;
+    for (size_t s = 0; s < order.size(); ++s) {
+      const int a = order[s];
+      const bool last = s + 1 == order.size();
+      int64_t prefix = 1, rest = 1;
+      for (int b = 0; b < a; ++b) prefix *= sz[b];
+      for (int b = a + 1; b < m; ++b) rest *= sz[b];
+      const int64_t nin = sz[a], nout = adj ? f[a]->cols : f[a]->rows;
+      Blk dst;
+      if (last) {
+        dst = y;
+      } else {
+        Geo gt;
+        gt.n2 = O;
+        gt.inner = ic;
+        dst = c.alloc_blk(c.dt, gt, prefix * nout * rest);
+      }
+      Geo gm;
+      gm.n1 = O;
+      gm.n2 = prefix;
+      gm.inner = rest * ic;
+      Blk xv = cur, yv = dst;
+      xv.s1 = cur.s2; xv.s2 = nin * rest * ic; xv.si = rest * ic;
+      yv.s1 = dst.s2; yv.s2 = nout * rest * ic; yv.si = rest * ic;
+      f[a]->apply(c, adj, xv, yv, gm, last ? acc : false);
+      sz[a] = nout;
+      cur = dst;
+    }
+  }
+};
+
+// Partial(base, rows, cols) (composites.py:239-320): scatter -> base -> gather.
+struct PartialNode : Node {
+  Node* base = nullptr;
+  DevBuf* ridx = nullptr;  // may be null (all rows)
+  DevBuf* cidx = nullptr;
+  bool r_unique = true, c_unique = true;
+  std::string describe() const override { return "Partial(" + base->describe() + ")"; }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, adj ? rows : cols);
+    DevBuf* in_idx = adj ? ridx : cidx;    // scatter side
+    DevBuf* out_idx = adj ? cidx : ridx;   // gather side
+    const bool in_unique = adj ? r_unique : c_unique;
+    const int64_t base_in = adj ? base->rows : base->cols;
+    const int64_t base_out = adj ? base->cols : base->rows;
+    Blk full_in = x;
+    if (in_idx) {
+      full_in = c.alloc_blk(c.dt, g, base_in);
+      PointArgs z;
+      z.y = full_in.p; z.y_dt = c.dt;
+      z.ys1 = full_in.s1; z.ys2 = full_in.s2; z.ysi = full_in.si;
+      z.n2 = g.n2; z.inner = g.inner; z.nb = g.count(); z.n = base_in;
+      c.point(z);
+      IndexArgs s;
+      s.x = x.p; s.xs1 = x.s1; s.xs2 = x.s2; s.xsi = x.si;
+      s.y = full_in.p; s.ys1 = full_in.s1; s.ys2 = full_in.s2; s.ysi = full_in.si;
+      s.n2 = g.n2; s.inner = g.inner; s.nb = g.count(); s.n = in_idx->len;
+      s.idx = (const int64_t*)in_idx->p;
+      s.atomic = !in_unique;
+      c.scatter(s);
+    }
+    if (!out_idx) {
+      base->apply(c, adj, full_in, y, g, acc);
+    } else {
+      Blk full_out = c.alloc_blk(c.dt, g, base_out);
+      base->apply(c, adj, full_in, full_out, g, false);
+      Blk dst = y;
+      if (acc) dst = c.alloc_blk(c.dt, g, out_idx->len);
+      IndexArgs s;
+      s.x = full_out.p; s.xs1 = full_out.s1; s.xs2 = full_out.s2; s.xsi = full_out.si;
+      s.y = dst.p; s.ys1 = dst.s1; s.ys2 = dst.s2; s.ysi = dst.si;
+      s.n2 = g.n2; s.inner = g.inner; s.nb = g.count(); s.n = out_idx->len;
+      s.idx = (const int64_t*)out_idx->p;
+      c.gather(s);
+      if (acc) point_copy(c, dst, y, g, out_idx->len, true);
+    }
+    c.release(m0);
+  }
+};
+
+// BlockDiag(*blocks) (composites.py:196-236).
+struct BlockDiagNode : Node {
+  std::vector<Node*> b;
+  std::string describe() const override { return "BlockDiag(" + std::to_string(b.size()) + " blocks)"; }
+  bool accepts_real() const override {
+    for (Node* n : b)
+      if (!n->accepts_real()) return false;
+    return true;
+  }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    int64_t ri = 0, ro = 0;
+    for (Node* n : b) {
+      const int64_t nin = adj ? n->rows : n->cols, nout = adj ? n->cols : n->rows;
+      n->apply(c, adj, offset_rows(x, ri), offset_rows(y, ro), g, acc);
+      ri += nin;
+      ro += nout;
+    }
+  }
+};
+
+// Blocks(grid) (composites.py:124-193).
+struct BlocksNode : Node {
+  int gr = 0, gc = 0;
+  std::vector<Node*> cells;  // row-major grid
+  std::string describe() const override {
+    return "Blocks(" + std::to_string(gr) + "x" + std::to_string(gc) + ")";
+  }
+  bool accepts_real() const override {
+    for (Node* n : cells)
+      if (!n->accepts_real()) return false;
+    return true;
+  }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    // fwd: y_i = sum_j A_ij x_j ; adj: y_j = sum_i A_ij^H x_i
+    const int no = adj ? gc : gr, ni = adj ? gr : gc;
+    int64_t ro = 0;
+    for (int o = 0; o < no; ++o) {
+      int64_t ri = 0, hout = 0;
+      for (int i = 0; i < ni; ++i) {
+        Node* n = adj ? cells[size_t(i) * gc + o] : cells[size_t(o) * gc + i];
+        const int64_t nin = adj ? n->rows : n->cols;
+        hout = adj ? n->cols : n->rows;
+        n->apply(c, adj, offset_rows(x, ri), offset_rows(y, ro), g, acc || i > 0);
+        ri += nin;
+      }
+      ro += hout;
+    }
+  }
+};
+
+// alpha * base (dparam = alpha): the scaled inverse DFT of kernels.dft and the
+// building block of polynomial operators.
+struct ScaledNode : Node {
+  Node* base = nullptr;
+  double re = 1.0, im = 0.0;
+  std::string describe() const override { return "Scaled(" + base->describe() + ")"; }
+  bool accepts_real() const override { return base->accepts_real(); }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    const double sim = adj ? -im : im;
+    const int64_t nout = adj ? cols : rows;
+    if (!acc) {
+      base->apply(c, adj, x, y, g, false);
+      point_copy(c, y, y, g, nout, false, nullptr, false, false, re, sim);
+      return;
+    }
+    const size_t m0 = c.mark();
+    Blk t = c.alloc_blk(c.dt, g, nout);
+    base->apply(c, adj, x, t, g, false);
+    point_copy(c, t, y, g, nout, true, nullptr, false, false, re, sim);
+    c.release(m0);
+  }
+};
+
+// ====================================================== plan building =====
+// Device FFT of a complex128 vector (plan-build helper: spectra, Bluestein).
+void device_fft_c128(Plan& p, int64_t n, const void* in_dev, void* out_dev) {
+  SMAT_CHECK(is_pow2(n), SMAT_NOT_POW2, "device_fft_c128 needs a power of two");
+  Ctx c;
+  c.device = p.device;
+  c.dt = SMAT_C128;
+  c.measure = true;
+  Blk x, y;
+  x.p = (void*)in_dev; x.dt = SMAT_C128; x.si = 1; x.s1 = x.s2 = n;
+  y.p = out_dev; y.dt = SMAT_C128; y.si = 1; y.s1 = y.s2 = n;
+  Geo g;
+  XformIO io;
+  io.x = x; io.x_rows = n; io.y = y; io.y_rows = n;
+  run_xform(c, n, g, io);
+  const size_t need = c.peak;
+  void* ws = nullptr;
+  if (need) SMAT_CUDA(cudaMalloc(&ws, need));
+  c.measure = false;
+  c.top = c.peak = 0;
+  c.ws = (char*)ws;
+  c.ws_size = need;
+  try {
+    run_xform(c, n, g, io);
+    SMAT_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    if (ws) cudaFree(ws);
+    throw;
+  }
+  if (ws) cudaFree(ws);
+}
+
+__global__ void chirp_kernel(double2* chirp, int64_t n) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+    // w_j = exp(-i pi (j^2 mod 2n) / n), exact integer reduction (kernels.py:86-87)
+    const unsigned long long r = (unsigned long long)(j) * (unsigned long long)(j) % (unsigned long long)(2 * n);
+    double s, c;
+    sincospi(-double(r) / double(n), &s, &c);
+    chirp[j] = make_double2(c, s);
+  }
+}
+__global__ void bluestein_kernel_fill(const double2* chirp, double2* ker, int64_t n, int64_t M) {
+  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < M; m += int64_t(gridDim.x) * blockDim.x) {
+    double2 v = make_double2(0, 0);
+    if (m < n) v = make_double2(chirp[m].x, -chirp[m].y);
+    else if (m > M - n) v = make_double2(chirp[M - m].x, -chirp[M - m].y);
+    ker[m] = v;
+  }
+}
+
+struct Builder {
+  Plan& p;
+  const smat_node* nodes;
+  int n_nodes;
+  const int32_t* children;
+  int n_children;
+  int depth = 0;
+
+  Node* child(const smat_node& nd, int k) {
+    SMAT_CHECK(nd.first_child >= 0 && nd.first_child + k < n_children, SMAT_BAD_ARG, "bad child index");
+    return build(children[nd.first_child + k]);
+  }
+
+  template <class T> T* add() {
+    auto u = std::make_unique<T>();
+    T* r = u.get();
+    p.nodes.push_back(std::move(u));
+    return r;
+  }
+
+  std::vector<Node*> memo;  // shared sub-operators are compiled once
+
+  Node* build(int idx) {
+    SMAT_CHECK(idx >= 0 && idx < n_nodes, SMAT_BAD_ARG, "bad node index");
+    if (memo.empty()) memo.assign(size_t(n_nodes), nullptr);
+    if (memo[size_t(idx)]) return memo[size_t(idx)];
+    SMAT_CHECK(++depth < 256, SMAT_BAD_ARG, "operator tree too deep");
+    const smat_node& nd = nodes[idx];
+    Node* out = nullptr;
+    const int cdt = dt_int(p.dt) ? -1 : cplx_of(p.dt);
+    switch (nd.kind) {
+      case SMAT_IDENTITY: out = add<IdentityNode>(); break;
+      case SMAT_ZERO: out = add<ZeroNode>(); break;
+      case SMAT_DIAGONAL: {
+        auto* n = add<DiagNode>();
+        n->d = upload_param(p, nd.param[0], p.dt);
+        out = n;
+        break;
+      }
+      case SMAT_DENSE: {
+        auto* n = add<DenseNode>();
+        SMAT_CHECK(nd.param[0].len == nd.rows * nd.cols, SMAT_BAD_SHAPE, "dense entries size");
+        n->A = upload_param(p, nd.param[0], p.dt);
+        out = n;
+        break;
+      }
+      case SMAT_LOWRANK: {
+        auto* n = add<LowRankNode>();
+        n->r = nd.iparam[0];
+        SMAT_CHECK(n->r >= 1 && nd.param[0].len == nd.rows * n->r && nd.param[1].len == nd.cols * n->r,
+                   SMAT_BAD_SHAPE, "lowrank factor sizes");
+        n->U = upload_param(p, nd.param[0], p.dt);
+        n->V = upload_param(p, nd.param[1], p.dt);
+        if (nd.param[2].len) n->s = upload_param(p, nd.param[2], p.dt);
+        out = n;
+        break;
+      }
+      case SMAT_HADAMARD: {
+        auto* n = add<HadamardNode>();
+        n->order = int(nd.iparam[0]);
+        SMAT_CHECK(n->order >= 0 && n->order <= 30, SMAT_BAD_ARG, "hadamard order");
+        out = n;
+        break;
+      }
+      case SMAT_FOURIER: {
+        SMAT_CHECK(cdt >= 0, SMAT_BAD_DTYPE, "Fourier needs a complex plan");
+        auto* n = add<FourierNode>();
+        n->n = nd.rows;
+        if (!is_pow2(n->n)) {
+          n->M = next_pow2(2 * n->n - 1);
+          DevBuf* ch = new_buf(p, SMAT_C128, n->n);
+          chirp_kernel<<<1184, 256>>>((double2*)ch->p, n->n);
+          SMAT_CUDA(cudaGetLastError());
+          DevBuf* ker = new_buf(p, SMAT_C128, n->M);
+          bluestein_kernel_fill<<<1184, 256>>>((const double2*)ch->p, (double2*)ker->p, n->n, n->M);
+          SMAT_CUDA(cudaGetLastError());
+          DevBuf* ks = new_buf(p, SMAT_C128, n->M);
+          device_fft_c128(p, n->M, ker->p, ks->p);
+          n->chirp = narrow_c128(p, ch, cdt);
+          n->kspec = narrow_c128(p, ks, cdt);
+        }
+        out = n;
+        break;
+      }
+      case SMAT_CIRCULANT: {
+        SMAT_CHECK(cdt >= 0, SMAT_BAD_DTYPE, "Circulant needs a floating plan");
+        const int64_t n = nd.rows;
+        SMAT_CHECK(nd.param[0].len == n, SMAT_BAD_SHAPE, "circulant column length");
+        if (is_pow2(n)) {
+          auto* c = add<CirculantNode>();
+          c->n = n;
+          DevBuf* cc = upload_param(p, nd.param[0], SMAT_C128);
+          DevBuf* sp = new_buf(p, SMAT_C128, n);
+          device_fft_c128(p, n, cc->p, sp->p);
+          c->spec = narrow_c128(p, sp, cdt);
+          out = c;
+        } else {
+          // C[i,j] = c[(i-j) mod n] == Toeplitz(c, [c[n-1], ..., c[1]]):
+          // linear-convolution embedding of length next_pow2(2n-1).
+          auto h = convert_host(nd.param[0], SMAT_C128);
+          const std::complex<double>* cv = (const std::complex<double>*)h.data();
+          auto* t = add<ToeplitzNode>();
+          t->L = next_pow2(2 * n - 1);
+          std::vector<std::complex<double>> e(size_t(t->L), 0.0);
+          for (int64_t i = 0; i < n; ++i) e[size_t(i)] = cv[i];
+          for (int64_t j = 1; j < n; ++j) e[size_t(t->L - j)] = cv[n - j];
+          DevBuf* eb = new_buf(p, SMAT_C128, t->L);
+          SMAT_CUDA(cudaMemcpy(eb->p, e.data(), e.size() * 16, cudaMemcpyHostToDevice));
+          DevBuf* sp = new_buf(p, SMAT_C128, t->L);
+          device_fft_c128(p, t->L, eb->p, sp->p);
+          t->spec = narrow_c128(p, sp, cdt);
+          out = t;
+        }
+        break;
+      }
+      case SMAT_TOEPLITZ: {
+        SMAT_CHECK(cdt >= 0, SMAT_BAD_DTYPE, "Toeplitz needs a floating plan");
+        auto* t = add<ToeplitzNode>();
+        const int64_t n = nd.rows, m = nd.cols;
+        SMAT_CHECK(nd.param[0].len == n && nd.param[1].len == m - 1, SMAT_BAD_SHAPE, "toeplitz sizes");
+        t->L = next_pow2(n + m - 1);
+        auto hc = convert_host(nd.param[0], SMAT_C128);
+        std::vector<std::complex<double>> e(size_t(t->L), 0.0);
+        const std::complex<double>* cv = (const std::complex<double>*)hc.data();
+        for (int64_t i = 0; i < n; ++i) e[size_t(i)] = cv[i];
+        if (m > 1) {
+          auto hr = convert_host(nd.param[1], SMAT_C128);
+          const std::complex<double>* rv = (const std::complex<double>*)hr.data();
+          // embed[L-(m-1):] = row_rest[::-1]  (leaves.py:258-259)
+          for (int64_t k = 0; k < m - 1; ++k) e[size_t(t->L - (m - 1) + k)] = rv[m - 2 - k];
+        }
+        DevBuf* eb = new_buf(p, SMAT_C128, t->L);
+        SMAT_CUDA(cudaMemcpy(eb->p, e.data(), e.size() * 16, cudaMemcpyHostToDevice));
+        DevBuf* sp = new_buf(p, SMAT_C128, t->L);
+        device_fft_c128(p, t->L, eb->p, sp->p);
+        t->spec = narrow_c128(p, sp, cdt);
+        out = t;
+        break;
+      }
+      case SMAT_ADJOINT: {
+        auto* a = add<AdjointNode>();
+        a->base = child(nd, 0);
+        out = a;
+        break;
+      }
+      case SMAT_PRODUCT: {
+        auto* a = add<ProductNode>();
+        for (int k = 0; k < nd.n_children; ++k) a->f.push_back(child(nd, k));
+        SMAT_CHECK(!a->f.empty(), SMAT_BAD_ARG, "empty product");
+        for (size_t k = 0; k + 1 < a->f.size(); ++k)
+          SMAT_CHECK(a->f[k]->cols == a->f[k + 1]->rows, SMAT_BAD_SHAPE, "product chain mismatch");
+        out = a;
+        break;
+      }
+      case SMAT_SUM: {
+        auto* a = add<SumNode>();
+        for (int k = 0; k < nd.n_children; ++k) a->t.push_back(child(nd, k));
+        SMAT_CHECK(!a->t.empty(), SMAT_BAD_ARG, "empty sum");
+        out = a;
+        break;
+      }
+      case SMAT_KRON: {
+        auto* a = add<KronNode>();
+        for (int k = 0; k < nd.n_children; ++k) a->f.push_back(child(nd, k));
+        SMAT_CHECK(a->f.size() >= 2, SMAT_BAD_ARG, "kron needs two factors");
+        out = a;
+        break;
+      }
+      case SMAT_PARTIAL: {
+        auto* a = add<PartialNode>();
+        a->base = child(nd, 0);
+        if (nd.iparam[0]) {
+          a->ridx = upload_param(p, nd.param[0], SMAT_I64);
+          a->r_unique = nd.iparam[2] != 0;
+        }
+        if (nd.iparam[1]) {
+          a->cidx = upload_param(p, nd.param[1], SMAT_I64);
+          a->c_unique = nd.iparam[3] != 0;
+        }
+        out = a;
+        break;
+      }
+      case SMAT_BLOCKDIAG: {
+        auto* a = add<BlockDiagNode>();
+        for (int k = 0; k < nd.n_children; ++k) a->b.push_back(child(nd, k));
+        out = a;
+        break;
+      }
+      case SMAT_BLOCKS: {
+        auto* a = add<BlocksNode>();
+        a->gr = int(nd.iparam[0]);
+        a->gc = int(nd.iparam[1]);
+        SMAT_CHECK(a->gr * a->gc == nd.n_children && a->gr > 0, SMAT_BAD_ARG, "blocks grid");
+        for (int k = 0; k < nd.n_children; ++k) a->cells.push_back(child(nd, k));
+        out = a;
+        break;
+      }
+      case SMAT_SCALED: {
+        auto* a = add<ScaledNode>();
+        a->base = child(nd, 0);
+        a->re = nd.dparam[0];
+        a->im = nd.dparam[1];
+        SMAT_CHECK(dt_complex(p.dt) || a->im == 0.0, SMAT_BAD_DTYPE, "complex scale in a real plan");
+        out = a;
+        break;
+      }
+      default:
+        throw Error(SMAT_UNSUPPORTED, "operator kind " + std::to_string(nd.kind) + " has no device path");
+    }
+    out->rows = nd.rows;
+    out->cols = nd.cols;
+    --depth;
+    memo[size_t(idx)] = out;
+    return out;
+  }
+};
+
+Plan* build_plan(const smat_node* nodes, int n_nodes, const int32_t* children, int n_children, int root,
+                 int dt, int device) {
+  SMAT_CHECK(dt >= SMAT_F32 && dt <= SMAT_I64, SMAT_BAD_DTYPE, "plan dtype");
+  auto p = std::make_unique<Plan>();
+  p->dt = dt;
+  p->device = device;
+  Builder b{*p, nodes, n_nodes, children, n_children};
+  p->root = b.build(root);
+  p->rows = p->root->rows;
+  p->cols = p->root->cols;
+  SMAT_CUDA(cudaDeviceSynchronize());
+  return p.release();
+}
+
+void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, void* y, int64_t ncols) {
+  const bool adj = dir == 1;
+  const int64_t nin = adj ? p.rows : p.cols, nout = adj ? p.cols : p.rows;
+  Geo g;
+  g.inner = ncols;
+  Blk xb;
+  xb.p = (void*)x;
+  xb.dt = x_dt;
+  xb.si = ncols;
+  xb.s2 = xb.s1 = nin * ncols;
+  Blk yb;
+  yb.p = y;
+  yb.dt = p.dt;
+  yb.si = ncols;
+  yb.s2 = yb.s1 = nout * ncols;
+  if (x_dt != p.dt && !p.root->accepts_real()) xb = promote(c, xb, g, nin);
+  p.root->apply(c, adj, xb, yb, g, false);
+}
+
+}  // namespace smat

@@ -1,0 +1,147 @@
+// plan.cuh — compiled operator plans: the native replacement of the
+// reference's recursive _forward/_backward dispatch (composites.py:49-61,
+// 96-113, 171-187, 290-310; leaves.py:40-290).
+//
+// A plan is a tree of executable nodes built once from the serialised
+// smat_node array.  apply() walks the tree on the HOST, launching one fused
+// pass per leaf transform (or per group of leaves for the pattern-matched
+// fused plans in fused.cu) on a single stream; all buffers come from the
+// caller's workspace via a bump allocator whose high-water mark is found by
+// a dry run (Ctx::measure), so apply() never allocates.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "misc_kernels.cuh"
+#include "tile_kernels.cuh"
+
+namespace smat {
+
+// A buffer view: element (o1, o2, i, c) at p + (o1*s1 + o2*s2 + i*si + c) elements.
+struct Blk {
+  void* p = nullptr;
+  int dt = 0;
+  int64_t s1 = 0, s2 = 0, si = 0;
+};
+// Batch geometry shared by the input and output views of one node apply.
+struct Geo {
+  int64_t n1 = 1, n2 = 1, inner = 1;
+  int64_t count() const { return n1 * n2 * inner; }
+};
+
+inline Blk offset_rows(const Blk& b, int64_t rows) {
+  Blk r = b;
+  r.p = (char*)b.p + rows * b.si * int64_t(dt_size(b.dt));
+  return r;
+}
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int dt = 0;  // plan dtype
+  char* ws = nullptr;
+  size_t ws_size = 0, top = 0, peak = 0;
+  bool measure = false;
+  int64_t launches = 0;
+
+  void* alloc(size_t bytes) {
+    size_t off = (top + 255) & ~size_t(255);
+    top = off + bytes;
+    if (top > peak) peak = top;
+    if (measure) return (void*)(uintptr_t(0x1000) + off);  // never dereferenced
+    SMAT_CHECK(top <= ws_size, SMAT_BAD_ARG,
+               "workspace too small: need " + std::to_string(top) + " bytes, have " +
+                   std::to_string(ws_size));
+    return ws + off;
+  }
+  // contiguous [n1*n2][rows][inner] buffer of dtype dt
+  Blk alloc_blk(int dtype, const Geo& g, int64_t rows) {
+    Blk b;
+    b.dt = dtype;
+    b.si = g.inner;
+    b.s2 = rows * g.inner;
+    b.s1 = g.n2 * b.s2;
+    b.p = alloc(size_t(g.count()) * size_t(rows) * dt_size(dtype));
+    return b;
+  }
+  size_t mark() const { return top; }
+  void release(size_t m) { top = m; }
+
+  // counted launches (skipped in measure mode)
+  void fft(int cdt, int N, const FftArgs& a) {
+    ++launches;
+    if (!measure) launch_fft_tile(cdt, N, a, stream);
+  }
+  void wht(int d, int N, const WhtArgs& a) {
+    ++launches;
+    if (!measure) launch_wht_tile(d, N, a, stream);
+  }
+  void point(const PointArgs& a) {
+    ++launches;
+    if (!measure) launch_point(dt, a, stream);
+  }
+  void gather(const IndexArgs& a) {
+    ++launches;
+    if (!measure) launch_gather(dt, a, stream);
+  }
+  void scatter(const IndexArgs& a) {
+    ++launches;
+    if (!measure) launch_scatter_add(dt, a, stream);
+  }
+  void gemm(const GemmArgs& a) {
+    ++launches;
+    if (!measure) launch_gemm(dt, a, device, stream);
+  }
+};
+
+// A device array owned by a plan.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int dt = 0;
+  int64_t len = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct Node {
+  int64_t rows = 0, cols = 0;
+  virtual ~Node() = default;
+  // y (=, or += when acc) op(x) with op = A (adj == false) or A^H.  x has
+  // n_in = adj ? rows : cols rows, y has n_out rows; both share geometry g.
+  // x.dt is the plan dtype or, for a complex plan, its real dtype when
+  // accepts_real() is true; y.dt is the plan dtype.
+  virtual void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) = 0;
+  virtual bool accepts_real() const { return false; }
+  virtual bool is_identity() const { return false; }
+  virtual std::string describe() const = 0;
+};
+
+struct Plan {
+  std::vector<std::unique_ptr<Node>> nodes;
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+  Node* root = nullptr;
+  int dt = 0;
+  int device = 0;
+  int64_t rows = 0, cols = 0;
+  std::string fused;  // name of the pattern-matched fused plan, if any
+};
+
+// builders (plan.cu)
+Plan* build_plan(const smat_node* nodes, int n_nodes, const int32_t* children, int n_children,
+                 int root, int dt, int device);
+void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, void* y, int64_t ncols);
+
+// helpers shared with fused.cu
+DevBuf* upload_param(Plan& p, const smat_param& prm, int target_dt);
+DevBuf* new_buf(Plan& p, int dt, int64_t len);
+void device_fft_c128(Plan& p, int64_t n, const void* in_dev, void* out_dev);
+
+}  // namespace smat

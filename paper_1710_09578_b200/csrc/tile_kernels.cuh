@@ -1,0 +1,72 @@
+// tile_kernels.cuh — argument blocks and launchers of the tiled FFT / FWHT passes.
+#pragma once
+
+#include "common.cuh"
+
+namespace smat {
+
+// One tiled FFT pass: for every batch b of the view, a length-N forward DFT
+// along i, with fused prologue/epilogue:
+//   load : v = x[b, i]  (real promoted)  -> conj? -> * pre[g_in] -> conj if inv
+//   core : forward DFT (N points)      [mid: * spec[g_mid], conj, DFT again]
+//   store: conj if inv|mid -> * W_tw^(goff*k) (four-step) -> * post[g_out]
+//          -> conj? -> * scale -> y[b, k]  (= or +=, real part or complex)
+// with the "global" row indices g_in = goff + i*gin_stride,
+// g_out = goff + k*gout_stride, g_mid = goff + k*mid_stride and
+// goff = (b / g_div) % g_mod.  Rows with g_in >= n_valid_in load as zero
+// (zero padding, leaves.py:269-270, kernels.py:116-118) and rows with
+// g_out >= n_valid_out are not stored (truncation, leaves.py:273,
+// kernels.py:125).
+struct FftArgs {
+  const void* x = nullptr;
+  void* y = nullptr;
+  int64_t xs1 = 0, xs2 = 0, xsi = 0;
+  int64_t ys1 = 0, ys2 = 0, ysi = 0;
+  int64_t n2 = 1, inner = 1, nb = 0;
+  int64_t g_div = 1, g_mod = 1, gin_stride = 1, gout_stride = 1;
+  int64_t n_valid_in = INT64_MAX, n_valid_out = INT64_MAX;
+  const void* pre = nullptr;
+  const void* post = nullptr;
+  const void* mid = nullptr;
+  int64_t mid_stride = 1;
+  const void* tw = nullptr;     // W_4096^t table of the working precision
+  const void* tw_lo = nullptr;  // four-step twiddle W_Ntot^t, t < 2^tw_lo_bits
+  const void* tw_hi = nullptr;  // W_Ntot^(t << tw_lo_bits)
+  int64_t tw_mask = 0;          // Ntot - 1
+  int32_t tw_lo_bits = 0;
+  double scale = 1.0;
+  int32_t x_real = 0, y_real = 0, conj_x = 0, conj_y = 0, inv = 0, mid_conj = 0;
+  int32_t tw_on = 0, tw_inv = 0, accumulate = 0, pre_conj = 0, post_conj = 0;
+};
+
+// One tiled FWHT pass over the view (stride-1-first stage order).
+struct WhtArgs {
+  const void* x = nullptr;
+  void* y = nullptr;
+  int64_t xs1 = 0, xs2 = 0, xsi = 0;
+  int64_t ys1 = 0, ys2 = 0, ysi = 0;
+  int64_t n2 = 1, inner = 1, nb = 0;
+  int64_t g_div = 1, g_mod = 1, gin_stride = 1, gout_stride = 1;
+  int64_t n_valid_in = INT64_MAX, n_valid_out = INT64_MAX;
+  int32_t accumulate = 0;
+};
+
+constexpr int kTileMax = 4096;
+
+// Launch one FFT tile pass of length N (power of two, 2..4096) in precision
+// `cdt` (SMAT_C64 or SMAT_C128).
+void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s);
+// Launch one FWHT tile pass of length N (power of two, 2..4096) on dtype dt.
+void launch_wht_tile(int dt, int N, const WhtArgs& a, cudaStream_t s);
+
+// Device-resident W_4096^t table of the given precision on `device`.
+const void* twiddle4096(int device, bool dbl);
+// Device-resident four-step twiddle tables for length `ntot` (pow2).
+struct TwPair {
+  const void* lo;
+  const void* hi;
+  int lo_bits;
+};
+TwPair twiddle_pair(int device, int64_t ntot, bool dbl);
+
+}  // namespace smat

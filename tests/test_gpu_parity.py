@@ -1,0 +1,279 @@
+"""Device parity: libsmat.so (sm_100a) against the golden fixtures and the CPU oracle.
+
+Tolerances (north star): bit-exact for integer FWHT; relative L2 <= 1e-12
+for float64/complex128 and <= 1e-5 for float32/complex64 — over the whole
+block and, stricter, per column.  float64 FWHT is additionally bit-exact
+(same stride-1-first stage order as the reference, kernels.py:181-189).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1710_09578_b200 as sm
+from conftest import max_col_rel_l2, rel_l2
+from oracle import linop_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.complex64: 1e-5, np.float64: 1e-12, np.complex128: 1e-12}
+
+
+def _keys(d, prefix):
+    return sorted({k.split("/")[1] for k in d if k.startswith(prefix + "/")})
+
+
+def _close(got, ref, tol, what=""):
+    e1, e2 = rel_l2(got, ref), max_col_rel_l2(got, ref)
+    assert e1 <= tol and e2 <= tol, f"{what}: relL2 {e1:.3e} maxcol {e2:.3e} > {tol:.0e}"
+
+
+def _fb(g, key, op, tol=1e-12, single=False):
+    x, y = g[f"{key}/x"], g[f"{key}/y"]
+    if single:
+        x = x.astype(np.complex64 if np.iscomplexobj(x) else np.float32)
+        y = y.astype(np.complex64 if np.iscomplexobj(y) else np.float32)
+        tol = 1e-5
+    _close(op.forward(x), g[f"{key}/fwd"], tol, key + " fwd")
+    _close(op.backward(y), g[f"{key}/bwd"], tol, key + " bwd")
+
+
+# ------------------------------------------------------------- Hadamard -----
+def test_hadamard_golden_bit_exact(golden_ops):
+    g = golden_ops
+    for o in _keys(g, "hadamard"):
+        order = int(o.split("=")[1])
+        op = sm.Hadamard(order)
+        key = f"hadamard/{o}"
+        assert np.array_equal(op.forward(g[f"{key}/x"]), g[f"{key}/fwd"]), key
+        assert np.array_equal(op.backward(g[f"{key}/y"]), g[f"{key}/bwd"]), key
+        xi = g[f"hadamard_i32/{o}/x"]
+        yi = op.forward(xi)
+        assert yi.dtype == np.int32
+        assert np.array_equal(yi.astype(np.int64), g[f"hadamard_i32/{o}/y"].astype(np.int64)), key
+
+
+def test_c1_config_exact(golden_ops):
+    g = golden_ops
+    op = sm.Hadamard(10)
+    assert np.array_equal(op.forward(g["c1/X"]), g["c1/fwd"])
+    assert np.array_equal(op.backward(g["c1/X"]), g["c1/bwd"])
+    yi = op.forward(g["c1/Xi"])
+    assert yi.dtype == np.int32
+    assert np.array_equal(yi.astype(np.int64), g["c1/fwd_i32"].astype(np.int64))
+    # float32 inside tolerance
+    _close(op.forward(g["c1/X"].astype(np.float32)), g["c1/fwd"], 1e-5, "c1 f32")
+
+
+@pytest.mark.parametrize("order", [13, 16, 20])
+def test_hadamard_multipass_bit_exact(order):
+    rng = np.random.default_rng(order)
+    x = rng.standard_normal((1 << order, 3))
+    assert np.array_equal(sm.Hadamard(order).forward(x), orc.fwht(x))
+    xi = rng.integers(-50, 51, (1 << order, 2)).astype(np.int32)
+    assert np.array_equal(sm.Hadamard(order).forward(xi).astype(np.int64),
+                          orc.fwht(xi).astype(np.int64))
+
+
+def test_hadamard_complex_and_involution():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((256, 4)) + 1j * rng.standard_normal((256, 4))
+    h = sm.Hadamard(8)
+    assert np.array_equal(h.forward(x), orc.fwht(x))
+    _close(h.forward(h.forward(x)), 256 * x, 1e-13, "involution")
+
+
+# -------------------------------------------------- Fourier / Circulant -----
+def test_fourier_golden(golden_ops):
+    g = golden_ops
+    for n in _keys(g, "fourier"):
+        op = sm.Fourier(int(n.split("=")[1]))
+        _fb(g, f"fourier/{n}", op)
+        _fb(g, f"fourier/{n}", op, single=True)
+
+
+def test_dft_kernel_api(golden_kernels):
+    g = golden_kernels
+    for n in _keys(g, "dft"):
+        x = g[f"dft/{n}/x"]
+        _close(sm.dft(x), g[f"dft/{n}/fwd"], 1e-12, n)
+        _close(sm.dft(x, inverse=True), g[f"dft/{n}/inv"], 1e-12, n)
+    for o in _keys(g, "fwht"):
+        assert np.array_equal(sm.fwht(g[f"fwht/{o}/x"]), g[f"fwht/{o}/y"])
+    for n in _keys(g, "cconv"):
+        got = sm.circular_convolve(g[f"cconv/{n}/c"], g[f"cconv/{n}/x"])
+        assert got.dtype == np.float64
+        _close(got, g[f"cconv/{n}/y"], 1e-12, n)
+
+
+def test_circulant_golden(golden_ops):
+    g = golden_ops
+    for kind in ("circulant_rr", "circulant_cc"):
+        for n in _keys(g, kind):
+            key = f"{kind}/{n}"
+            op = sm.Circulant(g[f"{key}/c"])
+            _fb(g, key, op)
+            _fb(g, key, op, single=True)
+            if kind == "circulant_rr":
+                assert op.forward(g[f"{key}/x"]).dtype == np.float64
+
+
+def test_toeplitz_golden(golden_ops):
+    g = golden_ops
+    for i in _keys(g, "toeplitz"):
+        key = f"toeplitz/{i}"
+        op = sm.Toeplitz(g[f"{key}/col"], g[f"{key}/row"])
+        _fb(g, key, op)
+        _fb(g, key, op, single=True)
+
+
+def test_kron_golden(golden_ops):
+    g = golden_ops
+    for i, (o, f, _) in enumerate([(1, 2, 4), (2, 4, 8), (3, 8, 16)]):
+        key = f"kron/{i}"
+        op = sm.Kron(sm.Hadamard(o), sm.Fourier(f), sm.Circulant(g[f"{key}/c"]))
+        _fb(g, key, op)
+        _fb(g, key, op, single=True)
+
+
+def test_c5_chain_golden(golden_ops):
+    g = golden_ops
+    for n in _keys(g, "c5"):
+        key = f"c5/{n}"
+        N = int(n.split("=")[1])
+        order = (N - 1).bit_length()
+        idx = np.arange(N)
+        op = sm.Product(sm.Diag(g[f"{key}/d1"]), sm.Fourier(N), sm.Diag(g[f"{key}/d2"]),
+                        sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx),
+                               sm.LowRank(g[f"{key}/U"], g[f"{key}/V"])))
+        _fb(g, key, op)
+
+
+# ----------------------------------------------------- device tensors -------
+def test_torch_cuda_tensors_match_host_path():
+    import torch
+
+    rng = np.random.default_rng(7)
+    c = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
+    x = (rng.standard_normal((4096, 8)) + 1j * rng.standard_normal((4096, 8))).astype(np.complex64)
+    op = sm.Circulant(c)
+    host = op.forward(x)
+    dev = op.forward(torch.from_numpy(x).cuda())
+    assert dev.is_cuda and dev.dtype == torch.complex64
+    assert np.array_equal(dev.cpu().numpy(), host)
+    back = op.backward(dev)
+    _close(back.cpu().numpy(), orc.apply(orc.circulant(c), orc.apply(orc.circulant(c), x), 1), 1e-5, "bwd")
+    pinned = torch.from_numpy(x).pin_memory()
+    cpu_out = op.forward(pinned)
+    assert not cpu_out.is_cuda
+    assert np.array_equal(cpu_out.numpy(), host)
+
+
+def test_vector_input_and_empty_columns():
+    op = sm.Fourier(12)
+    x = np.arange(12.0)
+    y = op.forward(x)
+    assert y.shape == (12,) and y.dtype == np.complex128
+    _close(y, orc.dft(x), 1e-12, "vec")
+    e = op.forward(np.zeros((12, 0)))
+    assert e.shape == (12, 0)
+
+
+def test_large_four_step_fft_and_bluestein():
+    rng = np.random.default_rng(11)
+    for n in (1 << 14, 1 << 20, 100_003):
+        x = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
+        op = sm.Fourier(n)
+        _close(op.forward(x), orc.dft(x), 1e-12, f"F{n} fwd")
+        _close(op.backward(x), orc.dft(x, inverse=True) * n, 1e-12, f"F{n} bwd")
+        _close(op.forward(x.astype(np.complex64)), orc.dft(x), 1e-5, f"F{n} c64")
+
+
+def test_adjoint_identity_random_ops():
+    rng = np.random.default_rng(5)
+    ops = [sm.Fourier(1000), sm.Circulant(rng.standard_normal(5000)),
+           sm.Toeplitz(rng.standard_normal(300), rng.standard_normal(500)),
+           sm.Kron(sm.Hadamard(3), sm.Fourier(5), sm.Diag(rng.standard_normal(7) + 1j))]
+    for op in ops:
+        x = rng.standard_normal((op.cols, 3)) + 1j * rng.standard_normal((op.cols, 3))
+        y = rng.standard_normal((op.rows, 3)) + 1j * rng.standard_normal((op.rows, 3))
+        lhs = np.sum(np.conj(y) * op.forward(x))
+        rhs = np.sum(np.conj(op.backward(y)) * x)
+        assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(op.forward(x)) * np.linalg.norm(y), op
+
+
+def _random_tree(rng, depth):
+    """Random composition tree with its oracle twin (reference tests/test_composites.py:313-398)."""
+    if depth == 0:
+        kind = rng.choice(["dense", "diagonal", "fourier", "hadamard", "circulant", "toeplitz"])
+        n = int(rng.integers(2, 9))
+        if kind == "dense":
+            m = int(rng.integers(2, 9))
+            a = rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))
+            return sm.Dense(a), orc.dense(a)
+        if kind == "diagonal":
+            d = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+            return sm.Diagonal(d), orc.diagonal(d)
+        if kind == "fourier":
+            return sm.Fourier(n), orc.fourier(n)
+        if kind == "hadamard":
+            o = int(rng.integers(1, 4))
+            return sm.Hadamard(o), orc.hadamard(o)
+        if kind == "circulant":
+            c = rng.standard_normal(n)
+            return sm.Circulant(c), orc.circulant(c)
+        m = int(rng.integers(2, 9))
+        col, row = rng.standard_normal(n), rng.standard_normal(m - 1)
+        return sm.Toeplitz(col, row), orc.toeplitz(col, row)
+    kind = rng.choice(["product", "kron", "sum", "partial", "adjoint", "blockdiag"])
+    child, oc = _random_tree(rng, depth - 1)
+    if kind == "product":
+        d = rng.standard_normal(child.rows)
+        return sm.Product(sm.Diagonal(d), child), orc.product(orc.diagonal(d), oc)
+    if kind == "kron":
+        d = rng.standard_normal(2)
+        return sm.Kron(sm.Diagonal(d), child), orc.kron(orc.diagonal(d), oc)
+    if kind == "sum":
+        d = rng.standard_normal(child.cols)
+        if child.rows == child.cols:
+            return sm.Sum(child, sm.Diagonal(d)), orc.sum_(oc, orc.diagonal(d))
+        return sm.Sum(child, child), orc.sum_(oc, oc)
+    if kind == "partial":
+        rows = rng.integers(0, child.rows, size=max(1, child.rows // 2))
+        return sm.Partial(child, row_indices=rows), orc.partial(oc, rows=rows)
+    if kind == "blockdiag":
+        other, oo = _random_tree(rng, 0)
+        return sm.BlockDiag(child, other), _orc_blockdiag(oc, oo)
+    return sm.Adjoint(child), (oc[1], oc[0], oc[3], oc[2], oc[4])
+
+
+def _orc_blockdiag(a, b):
+    def fwd(x):
+        return np.concatenate([a[0](x[: a[3]]), b[0](x[a[3]:])])
+
+    def bwd(y):
+        return np.concatenate([a[1](y[: a[2]]), b[1](y[a[2]:])])
+
+    return (fwd, bwd, a[2] + b[2], a[3] + b[3], a[4] and b[4])
+
+
+def test_fifty_random_trees():
+    rng = np.random.default_rng(2024)
+    for trial in range(50):
+        op, oc = _random_tree(rng, int(rng.integers(1, 4)))
+        x = rng.standard_normal((op.cols, 2)) + 1j * rng.standard_normal((op.cols, 2))
+        y = rng.standard_normal((op.rows, 2)) + 1j * rng.standard_normal((op.rows, 2))
+        _close(op.forward(x), orc.apply(oc, x, 0), 1e-12, f"tree {trial} fwd {op!r}")
+        _close(op.backward(y), orc.apply(oc, y, 1), 1e-12, f"tree {trial} bwd {op!r}")
+
+
+def test_to_dense_and_blocks():
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((3, 4))
+    b = rng.standard_normal((3, 2))
+    op = sm.Blocks([[sm.Dense(a), sm.Dense(b)], [sm.Zero(2, 4), sm.Identity(2)]])
+    ref = np.block([[a, b], [np.zeros((2, 4)), np.eye(2)]])
+    _close(op.to_dense(), ref, 1e-13, "blocks dense")
+    _close(sm.Hadamard(1).to_dense(), [[1, 1], [1, -1]], 0, "H1")
+    _close(sm.Fourier(2).to_dense(), [[1, 1], [1, -1]], 1e-15, "F2")
