@@ -1,0 +1,427 @@
+"""Benchmark of the structured-transform hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+
+Metric: forward/backward column throughput of one transform (columns/s) —
+one step = forward A·X then backward A^H·Y over the whole (rows, K) block of
+the workload, so value = 2K / step time (column-transforms per second, both
+directions counted).  Default workload: BASELINE config C2 (Circulant 2^20,
+64 complex64 columns) = configs[1]; c1..c5 select the others.
+
+Device timing: inputs resident in HBM, W untimed warm-up steps, then exactly
+K steps bracketed by barrier + cuda.synchronize, CUDA events on the launching
+stream, max over ranks.  Working sets exceed the 126 MB L2 for c2..c5; c1 is
+L2-flushed between steps (a 256 MB write).  Multi-GPU (torchrun): one process
+per GPU, every rank transforms its own full K-column block (weak scaling,
+column sharding, no collective on the data path; NCCL only for the barrier and
+the max-over-ranks timing reduction).
+
+Extra keys: e2e (the same metric through the public API with pinned HOST
+buffers, H2D+D2H inside the timed region), roofline (dominant kernel,
+algorithmic bytes per launch / its CUDA-event duration vs MEASURED_PEAKS.json),
+cpu_baseline (the CPU oracle — a numpy port of the reference algorithm — on a
+bounded sample on the host), gpu_launches, clocks.
+
+--impl reference: times the reference algorithm's CPU implementation (the
+oracle port; the reference is pure Python and cannot be installed on the GPU
+box) with all host cores (one process per column), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd/bwd columns/s and achieved HBM GB/s per transform vs B200 HBM peak"
+UNIT = "columns/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _workload_config(cfg: int):
+    from paper_1710_09578_b200 import configs
+
+    names = {1: "C1 Hadamard(10) 1024x16 float64", 2: "C2 Circulant(2^20) 2^20x64 complex64",
+             3: "C3 Toeplitz(3000x3000) 3000x4096 float32",
+             4: "C4 Kron(Hadamard(6),Fourier(128),Circulant(256)) 2^21x32 complex64",
+             5: "C5 Diag(d1)·Fourier(1000003)·Diag(d2)·Sum(Hpad,LowRank32) 1000003x128 complex128"}
+    dtypes = {1: "f64", 2: "c64", 3: "f32", 4: "c64", 5: "c128"}
+    return names[cfg], dtypes[cfg], configs
+
+
+# --------------------------------------------------------------- CPU legs ----
+def _oracle_op(cfg, w):
+    from oracle import linop_oracle as orc
+
+    p = w.params
+    if cfg == 1:
+        return orc.hadamard(p["order"])
+    if cfg == 2:
+        return orc.circulant(p["c"])
+    if cfg == 3:
+        return orc.toeplitz(p["col"], p["row_rest"])
+    if cfg == 4:
+        return orc.kron(orc.hadamard(p["h_order"]), orc.fourier(p["f_n"]), orc.circulant(p["c"]))
+    return orc.chain_c5(p["N"], p["d1"], p["d2"], p["U"], p["V"])
+
+
+# columns per CPU sample so one sample is ~10-30 s of single-core numpy work
+_SAMPLE_COLS = {1: 16, 2: 8, 3: 512, 4: 8, 5: 4}
+
+_POOL_STATE = {}
+
+
+def _pool_init(cfg):
+    from paper_1710_09578_b200 import configs
+
+    w = configs.make(cfg, ncols=1)
+    _POOL_STATE["w"] = w
+    _POOL_STATE["op"] = _oracle_op(cfg, w)
+    _POOL_STATE["cfg"] = cfg
+
+
+def _pool_column(j):
+    from oracle import linop_oracle as orc
+
+    w, op = _POOL_STATE["w"], _POOL_STATE["op"]
+    x = w.X[:, :1]
+    t0 = time.perf_counter()
+    y = orc.apply(op, x, 0)
+    orc.apply(op, y, 1)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg: int, cols: int | None = None):
+    """Single-core oracle (numpy port of the reference algorithm) on `cols` columns."""
+    from oracle import linop_oracle as orc
+    from paper_1710_09578_b200 import configs
+
+    cols = cols or _SAMPLE_COLS[cfg]
+    w = configs.make(cfg, ncols=cols)
+    op = _oracle_op(cfg, w)
+    orc.apply(op, w.X[:, :1], 0)  # warm the lru-cached plans (reference bench.py:263-270)
+    t0 = time.perf_counter()
+    y = orc.apply(op, w.X, 0)
+    orc.apply(op, y, 1)
+    dt = time.perf_counter() - t0
+    return {"value": 2 * cols / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{cols} of {_full_cols(cfg)} columns, forward then backward, "
+                      f"numpy oracle single-threaded ({dt:.2f} s)"}
+
+
+def _full_cols(cfg):
+    return {1: 16, 2: 64, 3: 4096, 4: 32, 5: 128}[cfg]
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm's CPU path with all host cores."""
+    import multiprocessing as mp
+
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    name, dtype, _ = _workload_config(cfg)
+    per_step = max(1, min(ncpu, _full_cols(cfg)))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(per_step, initializer=_pool_init, initargs=(cfg,)) as pool:
+        pool.map(_pool_column, range(per_step))  # warm-up: plans + page-in
+        for _ in range(max(0, args.warmup - 1)):
+            pool.map(_pool_column, range(per_step))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_pool_column, range(per_step))
+        dt = time.perf_counter() - t0
+    value = 2 * per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded numpy, SURVEY.md §8d)",
+        "config": {"workload": name, "columns_per_step": 2 * per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step, "kind": "port",
+                         "sample": f"{per_step} columns per step (one process per column), forward+backward, "
+                                   f"numpy port of the reference algorithm (oracle/linop_oracle.py)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU leg -----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [t.strip() for t in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        self.path.unlink(missing_ok=True)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _pass_bytes(cfg: int, label: str, ncols: int) -> int | None:
+    """Algorithmic bytes of one launch of the labelled kernel (SURVEY.md §8d units)."""
+    if cfg == 2:
+        n = 1 << 20
+        return 2 * n * ncols * 8 + (n * 8 if label == "mid" else 0)
+    if cfg == 4:
+        return 2 * (1 << 21) * ncols * 8
+    if cfg == 1:
+        return 2 * 1024 * ncols * 8
+    if cfg == 3:
+        return 2 * 3000 * ncols * 4
+    return None
+
+
+def _traffic(workload: str, kernel: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+    except (ValueError, AttributeError):
+        return None
+
+
+def run_native(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1710_09578_b200 as sm
+    from paper_1710_09578_b200 import configs
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    name, dtype, _ = _workload_config(cfg)
+    w = configs.make(cfg)
+    op = configs.operator(cfg, w)
+    K = w.ncols
+    X = torch.from_numpy(np.ascontiguousarray(w.X)).to(f"cuda:{dev}")
+    del w.X
+    stream = torch.cuda.current_stream(dev)
+
+    flush = None
+    if cfg == 1:  # working set < L2: flush between timed steps
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def step():
+        if flush is not None:
+            flush.fill_(1)
+        y = op.forward(X)
+        return op.backward(y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if flush is not None:  # subtract the flush writes, timed separately
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            flush.fill_(1)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms -= f0.elapsed_time(f1)
+    t = torch.tensor([ms], device=f"cuda:{dev}", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * 2 * K / (ms_step / 1e3)
+
+    # per-launch durations (CUDA events on the launching stream) for the roofline
+    plan = op.plan_for(w_dtype(cfg), dev)
+    pcode = plan.dtype_code
+    xcode = pcode
+    Y = op.forward(X)
+    launches = {0: plan.launches(0, K), 1: plan.launches(1, K)}
+    prof = []
+    for _ in range(max(3, min(args.steps, 10))):
+        prof += [("fwd",) + p for p in plan.apply_profiled(0, X, xcode, Y, K, stream.cuda_stream)]
+        Z = torch.empty_like(X)
+        prof += [("bwd",) + p for p in plan.apply_profiled(1, Y, xcode, Z, K, stream.cuda_stream)]
+    by_kernel = {}
+    for d, lab, t_ms in prof:
+        by_kernel.setdefault(lab, []).append(t_ms)
+    total = sum(sum(v) for v in by_kernel.values())
+    dom = max(by_kernel, key=lambda k: sum(by_kernel[k]))
+    dom_avg_ms = float(np.mean(by_kernel[dom]))
+    peak, peak_src = _peaks()
+    roofline = None
+    pb = _pass_bytes(cfg, "pass", K)
+    if pb is not None:
+        if cfg == 2:  # 3 launches per direction: 2 plain passes + the spectrum pass
+            pb = (3 * 2 * (1 << 20) * K * 8 + (1 << 20) * 8) / 3
+        achieved = pb / (dom_avg_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": _traffic(args.workload, dom),
+                    "bytes_per_launch": pb, "avg_launch_ms": dom_avg_ms,
+                    "share_of_step": sum(by_kernel[dom]) / total if total else None,
+                    "peak_source": peak_src}
+    alg = configs.algorithmic_bytes(cfg, K)
+    transform_gbs = 2 * alg / (ms_step / 1e3) / 1e9
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        e_steps = max(3, min(args.steps, 5))
+        yh = op.forward(Xh)
+        op.backward(yh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            yh = op.forward(Xh)
+            zh = op.backward(yh)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device=f"cuda:{dev}", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        bytes_in = Xh.numel() * Xh.element_size() + yh.numel() * yh.element_size()
+        bytes_out = yh.numel() * yh.element_size() + zh.numel() * zh.element_size()
+        e2e = {"value": world * 2 * K * e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(bytes_in),
+               "d2h_bytes_per_step": int(bytes_out), "steps": e_steps,
+               "path": "op.forward/op.backward on pinned CPU tensors (smat_apply_host, chunked H2D/compute/D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded numpy, SURVEY.md §8d)",
+            "config": {"workload": name, "columns_per_step": 2 * K, "global_columns": world * K,
+                       "parallelism": f"column-sharded x{world} (no data-path collective)",
+                       "l2": "inputs larger than L2" if cfg != 1 else "L2 flushed between steps (256 MB write)",
+                       "step": "forward + backward over the whole block"},
+            "transform_gbs": transform_gbs,
+            "algorithmic_bytes_per_direction": alg,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(args.steps * (launches[0] + launches[1])),
+            "launches_per_step": {"forward": launches[0], "backward": launches[1]},
+            "kernels_ms_per_step": {k: float(np.sum(v)) / max(3, min(args.steps, 10)) for k, v in by_kernel.items()},
+            "plan": plan.describe(),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def w_dtype(cfg):
+    return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
+
+
+def main():
+    args = _args()
+    cfg = int(args.workload[1])
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_native(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

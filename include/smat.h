@@ -166,6 +166,16 @@ SMAT_API int smat_apply(const smat_plan* plan, int32_t direction, const void* x,
 SMAT_API int smat_apply_host(const smat_plan* plan, int32_t direction, const void* x_host,
                     int32_t x_dtype, void* y_host, int64_t ncols, int32_t chunk_cols);
 
+/* smat_apply with a CUDA event recorded on `stream` before every launch and
+ * after the last one; synchronises the stream and returns the duration (ms) and
+ * a kernel label of each launch (at most `max_launches`; labels are written
+ * '\n'-separated into `labels`).  Measurement helper for bench.py's roofline. */
+SMAT_API int smat_apply_profiled(const smat_plan* plan, int32_t direction, const void* x,
+                                 int32_t x_dtype, void* y, int64_t ncols, void* workspace,
+                                 size_t workspace_bytes, void* stream, float* launch_ms,
+                                 int32_t max_launches, int32_t* n_launches, char* labels,
+                                 size_t labels_len);
+
 /* Number of kernel launches one smat_apply issues, and a human-readable
  * description of the compiled passes (diagnostics, bench gpu_launches). */
 SMAT_API int smat_plan_launches(const smat_plan* plan, int32_t direction, int64_t ncols,

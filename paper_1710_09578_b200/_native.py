@@ -98,6 +98,12 @@ _SIGNATURES = {
          ctypes.c_int32],
         ctypes.c_int,
     ),
+    "smat_apply_profiled": (
+        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float), ctypes.c_int32,
+         ctypes.POINTER(ctypes.c_int32), ctypes.c_char_p, ctypes.c_size_t],
+        ctypes.c_int,
+    ),
     "smat_plan_launches": (
         [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
         ctypes.c_int,
@@ -287,6 +293,23 @@ class Plan:
                                  ws.numel(), ctypes.c_void_p(stream_handle)),
             "smat_apply",
         )
+
+    def apply_profiled(self, direction: int, x, x_code: int, y, ncols: int, stream_handle: int):
+        """One smat_apply with per-launch CUDA events: [(label, ms), ...]."""
+        ws = self.workspace(direction, ncols)
+        cap = 256
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        labels = ctypes.create_string_buffer(cap * 32)
+        check(
+            self._lib.smat_apply_profiled(self.handle, direction, ctypes.c_void_p(x.data_ptr()), x_code,
+                                          ctypes.c_void_p(y.data_ptr()), ncols, ctypes.c_void_p(ws.data_ptr()),
+                                          ws.numel(), ctypes.c_void_p(stream_handle), ms, cap,
+                                          ctypes.byref(n), labels, len(labels)),
+            "smat_apply_profiled",
+        )
+        names = labels.value.decode().split("\n")
+        return [(names[i], float(ms[i])) for i in range(n.value)]
 
     # -- host path --------------------------------------------------------------
     def apply_host(self, direction: int, x_ptr: int, x_code: int, y_ptr: int, ncols: int,

@@ -2,6 +2,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "plan.cuh"
 
@@ -142,6 +143,45 @@ int smat_apply(const smat_plan* plan, int32_t direction, const void* x, int32_t 
     c.ws_size = workspace ? workspace_bytes : 0;
     smat::run_plan(p, c, direction, x, x_dtype, y, ncols);
   });
+}
+
+int smat_apply_profiled(const smat_plan* plan, int32_t direction, const void* x, int32_t x_dtype, void* y,
+                        int64_t ncols, void* workspace, size_t workspace_bytes, void* stream, float* launch_ms,
+                        int32_t max_launches, int32_t* n_launches, char* labels, size_t labels_len) {
+  if (!plan || !x || !y || !launch_ms || !n_launches) return fail(SMAT_BAD_ARG, "smat_apply_profiled: null argument");
+  if (direction != 0 && direction != 1) return fail(SMAT_BAD_ARG, "direction must be 0 or 1");
+  const smat::Plan& p = *plan->p;
+  if (x_dtype != p.dt && !(smat::dt_complex(p.dt) && x_dtype == smat::dt_real_of(p.dt)))
+    return fail(SMAT_BAD_DTYPE, "input dtype does not match the plan dtype");
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  int st = guarded([&] {
+    DeviceGuard dg(p.device);
+    smat::Ctx c;
+    c.device = p.device;
+    c.dt = p.dt;
+    c.stream = (cudaStream_t)stream;
+    c.ws = (char*)workspace;
+    c.ws_size = workspace ? workspace_bytes : 0;
+    c.prof = &ev;
+    smat::run_plan(p, c, direction, x, x_dtype, y, ncols);
+    c.note("end");
+    SMAT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    std::string lab;
+    int n = 0;
+    for (size_t i = 0; i + 1 < ev.size() && n < max_launches; ++i, ++n) {
+      float ms = 0.f;
+      SMAT_CUDA(cudaEventElapsedTime(&ms, ev[i].second, ev[i + 1].second));
+      launch_ms[n] = ms;
+      lab += ev[i].first + "\n";
+    }
+    *n_launches = n;
+    if (labels && labels_len) {
+      std::strncpy(labels, lab.c_str(), labels_len - 1);
+      labels[labels_len - 1] = 0;
+    }
+  });
+  for (auto& e : ev) cudaEventDestroy(e.second);
+  return st;
 }
 
 int smat_apply_host(const smat_plan* plan_c, int32_t direction, const void* x_host, int32_t x_dtype, void* y_host,

@@ -68,14 +68,43 @@ template <> struct RealOf<double2> { using T = double; };
 __host__ __device__ __forceinline__ float2 mk(float a, float b) { return make_float2(a, b); }
 __host__ __device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
 
-#define SMAT_CX_OPS(C)                                                               \
-  __host__ __device__ __forceinline__ C operator+(C a, C b) { return mk(a.x + b.x, a.y + b.y); } \
-  __host__ __device__ __forceinline__ C operator-(C a, C b) { return mk(a.x - b.x, a.y - b.y); } \
-  __host__ __device__ __forceinline__ C operator-(C a) { return mk(-a.x, -a.y); }               \
-  __host__ __device__ __forceinline__ C& operator+=(C& a, C b) { a.x += b.x; a.y += b.y; return a; }
-SMAT_CX_OPS(float2)
-SMAT_CX_OPS(double2)
-#undef SMAT_CX_OPS
+// complex64 add/sub use the packed FP32x2 pipe of sm_100 (FADD2): one
+// instruction per complex add instead of two.
+__host__ __device__ __forceinline__ float2 operator+(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+  return __fadd2_rn(a, b);
+#else
+  return mk(a.x + b.x, a.y + b.y);
+#endif
+}
+__host__ __device__ __forceinline__ float2 operator-(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+  return mk(a.x - b.x, a.y - b.y);
+#endif
+}
+__host__ __device__ __forceinline__ float2 operator-(float2 a) { return mk(-a.x, -a.y); }
+__host__ __device__ __forceinline__ float2& operator+=(float2& a, float2 b) { a = a + b; return a; }
+__host__ __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return mk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 operator-(double2 a, double2 b) { return mk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 operator-(double2 a) { return mk(-a.x, -a.y); }
+__host__ __device__ __forceinline__ double2& operator+=(double2& a, double2 b) { a.x += b.x; a.y += b.y; return a; }
+
+// d * (c - i s) for compile-time constants c, s
+__device__ __forceinline__ float2 mul_cs(float2 d, float c, float s) {
+  const float2 t = __fmul2_rn(d, make_float2(c, c));
+  return __ffma2_rn(make_float2(d.y, d.x), make_float2(s, -s), t);
+}
+__device__ __forceinline__ double2 mul_cs(double2 d, double c, double s) {
+  return make_double2(fma(d.x, c, d.y * s), fma(d.y, c, -d.x * s));
+}
+// a * w where q = (w.x, w.y, -w.y, w.x) (the "quad" twiddle layout of the
+// single-precision tables): FMUL2 + FFMA2.
+__device__ __forceinline__ float2 cmul_q(float2 a, float4 q) {
+  const float2 t = __fmul2_rn(make_float2(a.x, a.x), make_float2(q.x, q.y));
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(q.z, q.w), t);
+}
 
 __host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));

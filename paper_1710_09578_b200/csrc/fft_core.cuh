@@ -13,6 +13,11 @@
 // twiddles and keeps the reference's stage order (stride 1, 2, 4, ... — stride-1
 // first, kernels.py:181-189), which makes fp64 results bit-identical to the
 // reference and integer results exact.
+//
+// Shared-memory layout: element (row, column-slot cs) of a tile lives at
+// sm[(row + row/16) * CT + cs].  Skipping one row every 16 rows puts the rows
+// a warp touches in the radix-16 scatter (rows 16 apart) on different bank
+// halves/quarters, so every exchange runs at the 256-byte-per-warp minimum.
 #pragma once
 
 #include "common.cuh"
@@ -47,6 +52,9 @@ __host__ __device__ constexpr int st_ns(int N, int E, int s, bool mirror) {
   return m;
 }
 
+__device__ __forceinline__ int sm_row(int row) { return row + (row >> 4); }
+__host__ __device__ constexpr int sm_rows(int N) { return N + N / 16; }
+
 // ----------------------------------------------------- constant twiddles ---
 // d * W_16^t, W_16 = exp(-2*pi*i/16), t in [0, 8) known at compile time.
 template <class C>
@@ -54,15 +62,16 @@ __device__ __forceinline__ C mul_w16(C d, const int t) {
   using R = typename RealOf<C>::T;
   const R c1 = R(0.92387953251128675613), s1 = R(0.38268343236508977173),
           h = R(0.70710678118654752440);
+  // W_16^t = cos(2 pi t/16) - i sin(2 pi t/16)
   switch (t) {
     case 0: return d;
-    case 1: return mk(d.x * c1 + d.y * s1, d.y * c1 - d.x * s1);
-    case 2: return mk((d.x + d.y) * h, (d.y - d.x) * h);
-    case 3: return mk(d.x * s1 + d.y * c1, d.y * s1 - d.x * c1);
+    case 1: return mul_cs(d, c1, s1);
+    case 2: return mul_cs(d, h, h);
+    case 3: return mul_cs(d, s1, c1);
     case 4: return mk(d.y, -d.x);
-    case 5: return mk(d.y * c1 - d.x * s1, -(d.x * c1 + d.y * s1));
-    case 6: return mk((d.y - d.x) * h, -(d.x + d.y) * h);
-    default: return mk(d.y * s1 - d.x * c1, -(d.x * s1 + d.y * c1));
+    case 5: return mul_cs(d, -s1, c1);
+    case 6: return mul_cs(d, -h, h);
+    default: return mul_cs(d, -c1, s1);
   }
 }
 
@@ -72,13 +81,12 @@ __host__ __device__ constexpr int bitrev_c(int v, int bits) {
   return r;
 }
 __host__ __device__ constexpr int log2_c(int n) { return n <= 1 ? 0 : 1 + log2_c(n / 2); }
+__host__ __device__ constexpr int ctz_c(int v) { return (v & 1) ? 0 : 1 + ctz_c(v >> 1); }
 
-// In-register forward DFT of R = 2..16 points, natural order in and out.
+// In-register forward DFT of R = 1..16 points, natural order in and out.
 template <int R, class C>
 __device__ __forceinline__ void dft_small(C* a) {
-  if constexpr (R == 1) {
-    return;
-  } else {
+  if constexpr (R > 1) {
 #pragma unroll
     for (int half = R / 2; half >= 1; half >>= 1) {
 #pragma unroll
@@ -116,12 +124,56 @@ __device__ __forceinline__ void wht_small(T* a) {
   }
 }
 
+// a[r] *= w^r for r = 1..R-1 where wp[b] = w^(2^b) are table values: every
+// power is a product of at most log2(R) correctly rounded factors.
+template <int r, class C>
+__device__ __forceinline__ C power_of(const C* wp) {
+  constexpr int lo = ctz_c(r);
+  constexpr int rest = r & (r - 1);
+  C w = wp[lo];
+  if constexpr (rest & 2) w = cmul(w, wp[1]);
+  if constexpr (rest & 4) w = cmul(w, wp[2]);
+  if constexpr (rest & 8) w = cmul(w, wp[3]);
+  return w;
+}
+template <int R, int r = 1, class C>
+__device__ __forceinline__ void apply_powers(C* a, const C* wp) {
+  if constexpr (r < R) {
+    a[r] = cmul(a[r], power_of<r>(wp));
+    apply_powers<R, r + 1>(a, wp);
+  }
+}
+
+// a * W^t from a twiddle table: quad layout (float4) in single precision
+// (FMUL2 + FFMA2), plain double2 in double precision; TWS selects a shared-
+// memory table (plain loads) instead of the global one (__ldg).
+template <bool TWS>
+__device__ __forceinline__ float2 tw_mul(float2 a, const float2* tw, int t) {
+  const float4* q = reinterpret_cast<const float4*>(tw) + t;
+  return cmul_q(a, TWS ? *q : __ldg(q));
+}
+template <bool TWS>
+__device__ __forceinline__ double2 tw_mul(double2 a, const double2* tw, int t) {
+  return cmul(a, TWS ? tw[t] : __ldg(&tw[t]));
+}
+
+// Exchange-buffer row map.  LAY == 0: padded rows (row + row/16, the buffer
+// holds sm_rows(N) rows).  LAY = X > 0: dense rows permuted as
+// row ^ ((row >> 4) & (X - 1)) — X = rows per 128 bytes — so the radix-16
+// scatter (rows 16 apart) spreads over all bank groups without padding, which
+// lets a dense TMA landing buffer double as the exchange buffer.
+template <int LAY>
+__device__ __forceinline__ int ex_row(int row) {
+  if constexpr (LAY == 0) return row + (row >> 4);
+  else if constexpr (LAY == 1) return row;
+  else return row ^ ((row >> 4) & (LAY - 1));
+}
+
 // ------------------------------------------------- block FFT (Stockham) ----
 // Thread (j, cs) of a tile holds, at stage s (radix R, stride NS), the inputs
 // of butterflies bb = j + u*TPC (u < E/R): elements bb + r*N/R.  Outputs go to
-// (bb/NS)*NS*R + bb%NS + r*NS.  `sm` is the tile's shared buffer, element
-// (idx, cs) at sm[idx*CT + cs].  `tw` is W_4096^t (t < 4096).
-template <class C, int N, int E, int CT, bool MIR, int S>
+// (bb/NS)*NS*R + bb%NS + r*NS.  `tw` is W_TWN^t (t < TWN).
+template <class C, int N, int E, int CT, bool MIR, int S, int LAY = 0, int TWN = 4096, bool TWS = false>
 __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* __restrict__ tw) {
   constexpr int NST = st_count(N, E);
   if constexpr (S < NST) {
@@ -131,11 +183,11 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       if constexpr (NS > 1) {
-        const int bb = j + u * TPC;
-        const int k = bb & (NS - 1);
+        const int k = (j + u * TPC) & (NS - 1);
+        constexpr int step = TWN / (NS * R);
+        const int ks = k * step;
 #pragma unroll
-        for (int r = 1; r < R; ++r)
-          a[u * R + r] = cmul(a[u * R + r], __ldg(&tw[(r * k) * (4096 / (NS * R))]));
+        for (int r = 1; r < R; ++r) a[u * R + r] = tw_mul<TWS>(a[u * R + r], tw, r * ks);
       }
       dft_small<R>(a + u * R);
     }
@@ -148,16 +200,16 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
         const int k = bb & (NS - 1);
         const int base = (bb - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[(base + r * NS) * CT + cs] = a[u * R + r];
+        for (int r = 0; r < R; ++r) sm[ex_row<LAY>(base + r * NS) * CT + cs] = a[u * R + r];
       }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < E / R2; ++u) {
         const int bb = j + u * TPC;
 #pragma unroll
-        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[(bb + r * (N / R2)) * CT + cs];
+        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[ex_row<LAY>(bb + r * (N / R2)) * CT + cs];
       }
-      fft_stages<C, N, E, CT, MIR, S + 1>(a, sm, j, cs, tw);
+      fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS>(a, sm, j, cs, tw);
     }
   }
 }
@@ -181,7 +233,7 @@ __device__ __forceinline__ void wht_stages(T* a, T* sm, int j, int cs) {
         const int bb = j + u * TPC;
         const int base = (bb / NS) * (NS * R) + (bb % NS);
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[(base + r * NS) * CT + cs] = a[u * R + r];
+        for (int r = 0; r < R; ++r) sm[sm_row(base + r * NS) * CT + cs] = a[u * R + r];
       }
       __syncthreads();
 #pragma unroll
@@ -189,7 +241,7 @@ __device__ __forceinline__ void wht_stages(T* a, T* sm, int j, int cs) {
         const int bb = j + u * TPC;
         const int base = (bb / NS2) * (NS2 * R2) + (bb % NS2);
 #pragma unroll
-        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[(base + r * NS2) * CT + cs];
+        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[sm_row(base + r * NS2) * CT + cs];
       }
       wht_stages<T, N, E, CT, S + 1>(a, sm, j, cs);
     }

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(const GemmArgs a, int64_t k_c
   }
 }
 
-template <class P> static void gemm_go(const GemmArgs& a, int device, cudaStream_t s) {
+template <class P> static int gemm_go(const GemmArgs& a, int device, cudaStream_t s, bool dry) {
   const int64_t ntile = (a.inner + GBN - 1) / GBN;
   const int64_t mt = (a.m + GBM - 1) / GBM;
   const int64_t nbt = a.n1 * a.n2 * ntile;
@@ -274,6 +274,7 @@ template <class P> static void gemm_go(const GemmArgs& a, int device, cudaStream
   if (splits < 1) splits = 1;
   SMAT_CHECK(nbt < (int64_t(1) << 31) && mt < 65536, SMAT_UNSUPPORTED, "gemm grid too large");
   const int atomic_out = splits > 1;
+  if (dry) return (atomic_out && !a.accumulate) ? 2 : 1;
   if (atomic_out && !a.accumulate) {
     // zero the output view first
     PointArgs z;
@@ -286,15 +287,16 @@ template <class P> static void gemm_go(const GemmArgs& a, int device, cudaStream
   const dim3 grid_dims{unsigned(nbt), unsigned(mt), unsigned(splits)};
   gemm_kernel<P><<<grid_dims, 256, 0, s>>>(a, k_chunk, atomic_out);
   SMAT_CUDA(cudaGetLastError());
+  return (atomic_out && !a.accumulate) ? 2 : 1;
 }
 
-void launch_gemm(int dt, const GemmArgs& a, int device, cudaStream_t s) {
-  if (a.m == 0 || a.inner == 0 || a.n1 * a.n2 == 0) return;
+int launch_gemm(int dt, const GemmArgs& a, int device, cudaStream_t s, bool dry) {
+  if (a.m == 0 || a.inner == 0 || a.n1 * a.n2 == 0) return 0;
   switch (dt) {
-    case SMAT_F32: gemm_go<float>(a, device, s); break;
-    case SMAT_F64: gemm_go<double>(a, device, s); break;
-    case SMAT_C64: gemm_go<float2>(a, device, s); break;
-    case SMAT_C128: gemm_go<double2>(a, device, s); break;
+    case SMAT_F32: return gemm_go<float>(a, device, s, dry);
+    case SMAT_F64: return gemm_go<double>(a, device, s, dry);
+    case SMAT_C64: return gemm_go<float2>(a, device, s, dry);
+    case SMAT_C128: return gemm_go<double2>(a, device, s, dry);
     default: throw Error(SMAT_BAD_DTYPE, "gemm: unsupported dtype");
   }
 }

@@ -58,6 +58,7 @@ struct GemmArgs {
   const void* rowscale = nullptr;
   int32_t rowscale_conj = 0;
 };
-void launch_gemm(int dt, const GemmArgs& a, int device, cudaStream_t s);
+// Returns the number of kernels launched (counted only when dry).
+int launch_gemm(int dt, const GemmArgs& a, int device, cudaStream_t s, bool dry);
 
 }  // namespace smat

@@ -96,6 +96,37 @@ static DevBuf* narrow_c128(Plan& p, DevBuf* src, int cdt) {
   return d;
 }
 
+// Split of a four-step transform of length Nt = N1 * N2 (N1 = contiguous /
+// middle-pass length).  Must match run_xform.
+static void fourstep_split(int64_t Nt, int64_t& N1, int64_t& N2) {
+  const int l = ilog2(Nt);
+  N1 = int64_t(1) << ((l + 1) / 2);
+  N2 = Nt / N1;
+}
+
+__global__ void fourstep_perm_kernel(const double2* a, double2* b, int64_t N1, int64_t N2) {
+  const int64_t n = N1 * N2;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k2 = i / N1, k1 = i % N1;
+    b[i] = a[k2 + N2 * k1];
+  }
+}
+
+// A convolution spectrum as the plan stores it: four-step order when it is
+// longer than one tile (so the middle pass reads it contiguously per tile),
+// then narrowed to the plan's complex precision.
+static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
+  DevBuf* s = src;
+  if (src->len > kTileMax) {
+    int64_t N1, N2;
+    fourstep_split(src->len, N1, N2);
+    s = new_buf(p, SMAT_C128, src->len);
+    fourstep_perm_kernel<<<1184, 256>>>((const double2*)src->p, (double2*)s->p, N1, N2);
+    SMAT_CUDA(cudaGetLastError());
+  }
+  return narrow_c128(p, s, cdt);
+}
+
 // ------------------------------------------------------ view utilities -----
 // Merge (o1, o2) into a single outer index when both views allow it, so that
 // multi-pass transforms see n1 == 1.  Returns false when not mergeable.
@@ -278,7 +309,9 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.ys1 = W.s2; a.ys2 = N1 * ic; a.ysi = ic;
       a.n2 = N2; a.inner = ic; a.nb = O * N2 * ic;
       a.g_div = ic; a.g_mod = N2;
-      a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = N2;
+      // spectra longer than one tile are stored in four-step order
+      // (spec_fs[k2*N1 + k1] = spec[k2 + N2*k1], see spectrum_for_plan)
+      a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = 1; a.mid_gmul = N1;
       a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
       c.fft(cdt, int(N1), a);
     }
@@ -929,7 +962,7 @@ struct Builder {
           DevBuf* ks = new_buf(p, SMAT_C128, n->M);
           device_fft_c128(p, n->M, ker->p, ks->p);
           n->chirp = narrow_c128(p, ch, cdt);
-          n->kspec = narrow_c128(p, ks, cdt);
+          n->kspec = spectrum_for_plan(p, ks, cdt);
         }
         out = n;
         break;
@@ -944,7 +977,7 @@ struct Builder {
           DevBuf* cc = upload_param(p, nd.param[0], SMAT_C128);
           DevBuf* sp = new_buf(p, SMAT_C128, n);
           device_fft_c128(p, n, cc->p, sp->p);
-          c->spec = narrow_c128(p, sp, cdt);
+          c->spec = spectrum_for_plan(p, sp, cdt);
           out = c;
         } else {
           // C[i,j] = c[(i-j) mod n] == Toeplitz(c, [c[n-1], ..., c[1]]):
@@ -960,7 +993,7 @@ struct Builder {
           SMAT_CUDA(cudaMemcpy(eb->p, e.data(), e.size() * 16, cudaMemcpyHostToDevice));
           DevBuf* sp = new_buf(p, SMAT_C128, t->L);
           device_fft_c128(p, t->L, eb->p, sp->p);
-          t->spec = narrow_c128(p, sp, cdt);
+          t->spec = spectrum_for_plan(p, sp, cdt);
           out = t;
         }
         break;
@@ -985,7 +1018,7 @@ struct Builder {
         SMAT_CUDA(cudaMemcpy(eb->p, e.data(), e.size() * 16, cudaMemcpyHostToDevice));
         DevBuf* sp = new_buf(p, SMAT_C128, t->L);
         device_fft_c128(p, t->L, eb->p, sp->p);
-        t->spec = narrow_c128(p, sp, cdt);
+        t->spec = spectrum_for_plan(p, sp, cdt);
         out = t;
         break;
       }

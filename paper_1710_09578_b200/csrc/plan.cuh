@@ -70,30 +70,47 @@ struct Ctx {
   size_t mark() const { return top; }
   void release(size_t m) { top = m; }
 
+  // optional per-launch profiling (smat_apply_profiled): an event is recorded
+  // on the stream before every launch
+  std::vector<std::pair<std::string, cudaEvent_t>>* prof = nullptr;
+  void note(const std::string& name) {
+    if (!prof || measure) return;
+    cudaEvent_t e;
+    SMAT_CUDA(cudaEventCreate(&e));
+    SMAT_CUDA(cudaEventRecord(e, stream));
+    prof->emplace_back(name, e);
+  }
+
   // counted launches (skipped in measure mode)
   void fft(int cdt, int N, const FftArgs& a) {
     ++launches;
+    note(std::string(cdt == SMAT_C128 ? "fft_c128_" : "fft_c64_") + std::to_string(N));
     if (!measure) launch_fft_tile(cdt, N, a, stream);
   }
   void wht(int d, int N, const WhtArgs& a) {
     ++launches;
+    note("wht_" + std::to_string(N));
     if (!measure) launch_wht_tile(d, N, a, stream);
   }
   void point(const PointArgs& a) {
     ++launches;
+    note("point");
     if (!measure) launch_point(dt, a, stream);
   }
   void gather(const IndexArgs& a) {
     ++launches;
+    note("gather");
     if (!measure) launch_gather(dt, a, stream);
   }
   void scatter(const IndexArgs& a) {
     ++launches;
+    note("scatter");
     if (!measure) launch_scatter_add(dt, a, stream);
   }
   void gemm(const GemmArgs& a) {
-    ++launches;
-    if (!measure) launch_gemm(dt, a, device, stream);
+    launches += launch_gemm(dt, a, device, stream, true);
+    note("gemm");
+    if (!measure) launch_gemm(dt, a, device, stream, false);
   }
 };
 

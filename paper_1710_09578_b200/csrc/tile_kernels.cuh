@@ -29,6 +29,7 @@ struct FftArgs {
   const void* post = nullptr;
   const void* mid = nullptr;
   int64_t mid_stride = 1;
+  int64_t mid_gmul = 1;  // spectrum index = goff*mid_gmul + k*mid_stride
   const void* tw = nullptr;     // W_4096^t table of the working precision
   const void* tw_lo = nullptr;  // four-step twiddle W_Ntot^t, t < 2^tw_lo_bits
   const void* tw_hi = nullptr;  // W_Ntot^(t << tw_lo_bits)

@@ -1,0 +1,101 @@
+// tma.cuh — Tensor Memory Accelerator + mbarrier helpers (inline PTX, sm_100a).
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace smat {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 5-D tiled TMA load global -> shared, completion counted on `bar` (bytes).
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---------------------------------------------------------------- host -----
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Tensor map of a block view  element (o1, o2, i, c) at p + o1*s1 + o2*s2 + i*si + c
+// (element size esz, a multiple of 8 bytes), i < N split as (i % 256, i / 256),
+// box = CT columns x all N rows of one (o1, o2).
+inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n1, int64_t s1, int64_t n2,
+                          int64_t s2, int64_t N, int64_t si, int64_t inner, int CT) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int64_t w = int64_t(esz / 8);  // 8-byte words per element
+  const int64_t rlo = N < 256 ? N : 256, rhi = N / rlo;
+  cuuint64_t dims[5] = {cuuint64_t(inner * w), cuuint64_t(rlo), cuuint64_t(rhi), cuuint64_t(n2), cuuint64_t(n1)};
+  cuuint64_t strides[4] = {cuuint64_t(si * int64_t(esz)), cuuint64_t(256 * si * int64_t(esz)),
+                           cuuint64_t(s2 * int64_t(esz)), cuuint64_t(s1 * int64_t(esz))};
+  for (int k = 0; k < 4; ++k)
+    if (strides[k] % 16 || strides[k] >= (cuuint64_t(1) << 40)) {
+      if (!(k >= 1 && dims[k + 1] == 1)) return false;
+      strides[k] = 16;  // unused dimension of extent 1
+    }
+  if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return false;
+  cuuint32_t box[5] = {cuuint32_t(CT * w), cuuint32_t(rlo), cuuint32_t(rhi), 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<void*>(p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace smat
