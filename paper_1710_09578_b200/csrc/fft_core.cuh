@@ -56,23 +56,26 @@ __device__ __forceinline__ int sm_row(int row) { return row + (row >> 4); }
 __host__ __device__ constexpr int sm_rows(int N) { return N + N / 16; }
 
 // ----------------------------------------------------- constant twiddles ---
-// d * W_16^t, W_16 = exp(-2*pi*i/16), t in [0, 8) known at compile time.
+// d * W_32^t, W_32 = exp(-2*pi*i/32), t in [0, 16) known at compile time:
+// W_32^t = cos(pi t/16) - i sin(pi t/16).
 template <class C>
-__device__ __forceinline__ C mul_w16(C d, const int t) {
+__device__ __forceinline__ C mul_w32(C d, const int t) {
   using R = typename RealOf<C>::T;
-  const R c1 = R(0.92387953251128675613), s1 = R(0.38268343236508977173),
-          h = R(0.70710678118654752440);
-  // W_16^t = cos(2 pi t/16) - i sin(2 pi t/16)
-  switch (t) {
-    case 0: return d;
-    case 1: return mul_cs(d, c1, s1);
-    case 2: return mul_cs(d, h, h);
-    case 3: return mul_cs(d, s1, c1);
-    case 4: return mk(d.y, -d.x);
-    case 5: return mul_cs(d, -s1, c1);
-    case 6: return mul_cs(d, -h, h);
-    default: return mul_cs(d, -c1, s1);
-  }
+  constexpr double cs[9] = {1.0,
+                            0.98078528040323044913,
+                            0.92387953251128675613,
+                            0.83146961230254523708,
+                            0.70710678118654752440,
+                            0.55557023301960222474,
+                            0.38268343236508977173,
+                            0.19509032201612826785,
+                            0.0};
+  if (t == 0) return d;
+  if (t == 8) return mk(d.y, -d.x);
+  // cos(pi t/16) = cs[t] (t <= 8) or -cs[16 - t]; sin(pi t/16) = cs[8 - t] or cs[t - 8]
+  const R c = t <= 8 ? R(cs[t]) : R(-cs[16 - t]);
+  const R s = t <= 8 ? R(cs[8 - t]) : R(cs[t - 8]);
+  return mul_cs(d, c, s);
 }
 
 __host__ __device__ constexpr int bitrev_c(int v, int bits) {
@@ -83,7 +86,7 @@ __host__ __device__ constexpr int bitrev_c(int v, int bits) {
 __host__ __device__ constexpr int log2_c(int n) { return n <= 1 ? 0 : 1 + log2_c(n / 2); }
 __host__ __device__ constexpr int ctz_c(int v) { return (v & 1) ? 0 : 1 + ctz_c(v >> 1); }
 
-// In-register forward DFT of R = 1..16 points, natural order in and out.
+// In-register forward DFT of R = 1..32 points, natural order in and out.
 template <int R, class C>
 __device__ __forceinline__ void dft_small(C* a) {
   if constexpr (R > 1) {
@@ -95,7 +98,7 @@ __device__ __forceinline__ void dft_small(C* a) {
         for (int q = 0; q < half; ++q) {
           C x = a[blk + q], y = a[blk + q + half];
           a[blk + q] = x + y;
-          a[blk + q + half] = mul_w16(x - y, q * (16 / (2 * half)));
+          a[blk + q + half] = mul_w32(x - y, q * (32 / (2 * half)));
         }
       }
     }
@@ -134,6 +137,7 @@ __device__ __forceinline__ C power_of(const C* wp) {
   if constexpr (rest & 2) w = cmul(w, wp[1]);
   if constexpr (rest & 4) w = cmul(w, wp[2]);
   if constexpr (rest & 8) w = cmul(w, wp[3]);
+  if constexpr (rest & 16) w = cmul(w, wp[4]);
   return w;
 }
 template <int R, int r = 1, class C>
@@ -156,6 +160,14 @@ template <bool TWS>
 __device__ __forceinline__ double2 tw_mul(double2 a, const double2* tw, int t) {
   return cmul(a, TWS ? tw[t] : __ldg(&tw[t]));
 }
+
+// Spectrum entry i (plan layout: float4 quads for complex64, double2 for
+// complex128) as a plain complex value, and as the quad for cmul_q.
+__device__ __forceinline__ float2 ld_spec(const float2* mid, int64_t i) {
+  const float4 q = __ldg(reinterpret_cast<const float4*>(mid) + i);
+  return make_float2(q.x, q.y);
+}
+__device__ __forceinline__ double2 ld_spec(const double2* mid, int64_t i) { return __ldg(mid + i); }
 
 // Exchange-buffer row map.  LAY == 0: padded rows (row + row/16, the buffer
 // holds sm_rows(N) rows).  LAY = X > 0: dense rows permuted as

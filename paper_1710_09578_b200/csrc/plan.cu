@@ -112,9 +112,17 @@ __global__ void fourstep_perm_kernel(const double2* a, double2* b, int64_t N1, i
   }
 }
 
+__global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float c = float(a[i].x), s = float(a[i].y);
+    b[i] = make_float4(c, s, -s, c);
+  }
+}
+
 // A convolution spectrum as the plan stores it: four-step order when it is
 // longer than one tile (so the middle pass reads it contiguously per tile),
-// then narrowed to the plan's complex precision.
+// then in the plan's complex precision — double2 for complex128 plans, the
+// (w.x, w.y, -w.y, w.x) quad layout of cmul_q for complex64 plans.
 static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
   DevBuf* s = src;
   if (src->len > kTileMax) {
@@ -124,7 +132,11 @@ static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
     fourstep_perm_kernel<<<1184, 256>>>((const double2*)src->p, (double2*)s->p, N1, N2);
     SMAT_CUDA(cudaGetLastError());
   }
-  return narrow_c128(p, s, cdt);
+  if (cdt == SMAT_C128) return s;
+  DevBuf* q = new_buf(p, SMAT_C128, s->len);  // 16 bytes per entry
+  c128_to_quad_kernel<<<1184, 256>>>((const double2*)s->p, (float4*)q->p, s->len);
+  SMAT_CUDA(cudaGetLastError());
+  return q;
 }
 
 // ------------------------------------------------------ view utilities -----

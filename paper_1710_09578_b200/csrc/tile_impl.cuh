@@ -196,14 +196,15 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
   fft_stages<C, N, E, CT, false, 0>(a, sm, j, cs, tw);
   if constexpr (MID) {
     constexpr int RF = st_radix(N, E, NST - 1, false);
-    const C* mid = (const C*)p.mid + goff * p.mid_gmul;
+    const C* mid = (const C*)p.mid;
+    const int64_t mbase = int64_t(goff) * p.mid_gmul;
     const R sm_im = (f & F_MIDCONJ) ? R(-1) : R(1);
 #pragma unroll
     for (int u = 0; u < E / RF; ++u)
 #pragma unroll
       for (int r = 0; r < RF; ++r) {
         const int k = j + u * TPC + r * (N / RF);
-        C s = act ? __ldg(&mid[k * p.mid_stride]) : mk(R(0), R(0));
+        C s = act ? ld_spec(mid, mbase + k * p.mid_stride) : mk(R(0), R(0));
         s.y *= sm_im;
         a[u * RF + r] = conj(cmul(a[u * RF + r], s));
       }

@@ -21,26 +21,36 @@
 
 namespace smat {
 
-template <class C, int N>
+// EP: elements per thread (16 -> radix-16 stages, 32 -> radix-32 stages: one
+// exchange fewer for N = 1024); NB: landing buffers per CTA (0 = as many as fit,
+// up to 3).
+template <class C, int N, int EP = 16, int NB = 0, bool TV = false, bool MS = false>
 struct TmaGeom {
-  static constexpr int E = tile_E(N);
+  static constexpr int E = N < EP ? N : EP;
   static constexpr int CT = tile_CT(N, sizeof(C));
   static constexpr int TPC = N / E;
   static constexpr int T = TPC * CT;
   static constexpr int ROWB = CT * int(sizeof(C));                 // bytes per tile row
   static constexpr int LAY = ROWB >= 128 ? 1 : 128 / ROWB;          // exchange row permutation
   static constexpr size_t BUF = size_t(N) * CT * sizeof(C);         // one dense TMA box
+  static constexpr size_t SPB = MS ? size_t(N) * 16 : 0;           // the tile's spectrum slice
+  static constexpr size_t STAGE = BUF + SPB;
   static constexpr size_t TWB = size_t(N) * 16;                    // W_N (float4 quads / double2)
+  static constexpr size_t TVB = TV ? size_t(N) * 16 : 0;           // per-tile four-step twiddles
   // ring of landing buffers: tile t computes in one while t+1.. load into the others
-  static constexpr int NBUF = (227 * 1024 - int(TWB) - 64) / int(BUF) >= 3 ? 3 : 2;
-  static constexpr size_t SMEM = NBUF * BUF + TWB + 64;
+  static constexpr int NBUF =
+      NB > 0 && (227 * 1024 - int(TWB + TVB) - 64) / int(STAGE) >= NB
+          ? NB
+          : ((227 * 1024 - int(TWB + TVB) - 64) / int(STAGE) >= 3 ? 3 : 2);
+  static constexpr size_t SMEM = NBUF * STAGE + TWB + TVB + 64;
   static constexpr int MINB = (227 * 1024) / int(SMEM) >= 2 && 2 * T <= 1024 ? 2 : 1;
 };
 
-template <class C, int N, bool MID, bool TW>
-__global__ void __launch_bounds__(TmaGeom<C, N>::T, TmaGeom<C, N>::MINB)
-    fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FftDev p, const int ntiles) {
-  using G = TmaGeom<C, N>;
+template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS>
+__global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, N, EP, NB, TW, MID>::MINB)
+    fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                   const FftDev p, const int ntiles) {
+  using G = TmaGeom<C, N, EP, NB, TW, MID>;
   using R = typename RealOf<C>::T;
   constexpr int E = G::E, CT = G::CT, TPC = G::TPC, LAY = G::LAY;
   constexpr int NST = st_count(N, E);
@@ -48,9 +58,12 @@ __global__ void __launch_bounds__(TmaGeom<C, N>::T, TmaGeom<C, N>::MINB)
   constexpr int RL = MID ? st_radix(N, E, NST - 1, true) : st_radix(N, E, NST - 1, false);
   constexpr int LQ = log2_c(RL);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  C* bufs = reinterpret_cast<C*>(smem_raw);
-  C* tws = reinterpret_cast<C*>(smem_raw + G::NBUF * G::BUF);  // W_N^t, t < N (float4 quads or double2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::NBUF * G::BUF + G::TWB);
+  // stage s: [tile data | spectrum slice] at smem_raw + s*STAGE
+  auto stage_buf = [&](int s) { return reinterpret_cast<C*>(smem_raw + s * G::STAGE); };
+  auto stage_spec = [&](int s) { return smem_raw + s * G::STAGE + G::BUF; };
+  C* tws = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE);  // W_N^t, t < N (float4 quads or double2)
+  C* tvs = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE + G::TWB);  // four-step twiddles of the tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::NBUF * G::STAGE + G::TWB + G::TVB);
   const int tid = threadIdx.x, cs = tid % CT, j = tid / CT;
   const uint32_t f = p.flags;
   const R sx = ((f & F_CONJX) != 0) != (!MID && (f & F_INV)) ? R(-1) : R(1);
@@ -64,18 +77,48 @@ __global__ void __launch_bounds__(TmaGeom<C, N>::T, TmaGeom<C, N>::MINB)
   auto issue = [&](int t, int s) {
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
-    mbar_arrive_expect_tx(&bars[s], uint32_t(G::BUF));
-    tma_load_5d(bufs + s * (G::BUF / sizeof(C)), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2),
-                int(o1));
+    mbar_arrive_expect_tx(&bars[s], uint32_t(G::BUF + G::SPB));
+    tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
+    if constexpr (MID) {
+      // the tile's contiguous spectrum slice rides on the same barrier
+      const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
+      const uint32_t g = q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d;
+      bulk_load(stage_spec(s), reinterpret_cast<const unsigned char*>(p.mid) + size_t(g) * p.mid_gmul * 16,
+                uint32_t(G::SPB), &bars[s]);
+    }
   };
 
+  // tiles are dealt round-robin (tile t = blockIdx.x + i*gridDim.x): at any
+  // moment the CTAs work on neighbouring column groups of the same rows, so
+  // every DRAM page opened serves all of them
+  const int gs = int(gridDim.x);
   if (tid == 0) {
     tma_prefetch_desc(&xmap);
     for (int s = 0; s < G::NBUF; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
     for (int s = 0; s < G::NBUF; ++s)
-      if (int(blockIdx.x + s * gridDim.x) < ntiles) issue(blockIdx.x + s * gridDim.x, s);
+      if (int(blockIdx.x) + s * gs < ntiles) issue(blockIdx.x + s * gs, s);
   }
+  // four-step twiddle software pipeline: the two-level table lookups of the
+  // NEXT tile are issued during the current one
+  constexpr int PER = (N + G::T - 1) / G::T;
+  C tvlo[TW ? PER : 1], tvhi[TW ? PER : 1];
+  auto tv_prefetch = [&](int t) {
+    if constexpr (TW) {
+      const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
+      const uint32_t g32 = q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d;
+      const C* thi = (const C*)p.tw_hi;
+      const C* tlo = (const C*)p.tw_lo;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int k = tid + i * G::T;
+        const uint32_t m = (g32 * uint32_t(k < N ? k : 0)) & p.tw_mask;
+        tvhi[i] = __ldg(&thi[m >> p.tw_lo_bits]);
+        tvlo[i] = __ldg(&tlo[m & ((1u << p.tw_lo_bits) - 1u)]);
+      }
+    }
+  };
+  if (int(blockIdx.x) < ntiles) tv_prefetch(blockIdx.x);
   // shared copy of W_N from the global W_4096 table (stride 4096/N)
   {
     constexpr int st = 4096 / N;
@@ -90,9 +133,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N>::T, TmaGeom<C, N>::MINB)
   }
   __syncthreads();
 
-  for (int t = blockIdx.x, it = 0; t < ntiles; t += gridDim.x, ++it) {
-    // ---- per-thread batch geometry and four-step twiddles (latency hidden
-    //      behind the TMA wait and the transform)
+  for (int t = blockIdx.x, it = 0; t < ntiles; t += gs, ++it) {
+    // ---- per-thread batch geometry
     const uint32_t b = uint32_t(t) * CT + cs;
     uint32_t o1, o2, c;
     decode_batch(b, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c);
@@ -102,110 +144,199 @@ __global__ void __launch_bounds__(TmaGeom<C, N>::T, TmaGeom<C, N>::MINB)
       const uint32_t q = fdiv(b, p.gdiv.m, p.gdiv.s);
       goff = int32_t(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
     }
-    C wbase[E / RL];
-    C wp[LQ > 0 ? LQ : 1];
     if constexpr (TW) {
-      const uint32_t g32 = uint32_t(goff);
-      const C* thi = (const C*)p.tw_hi;
-      const C* tlo = (const C*)p.tw_lo;
+      // goff is uniform over the tile's CT columns (launcher checks): the
+      // twiddles W^(goff*k) (conjugated for the inverse) are shared by all
+      // columns — finish the lookups prefetched during the previous tile into
+      // shared memory (the previous epilogue's reads are fenced by its
+      // trailing barrier), then start the next tile's lookups.
 #pragma unroll
-      for (int q = 0; q < LQ; ++q) wp[q] = tw2<C>(thi, tlo, p.tw_mask, p.tw_lo_bits, g32 * uint32_t((N / RL) << q));
-#pragma unroll
-      for (int u = 0; u < E / RL; ++u)
-        wbase[u] = tw2<C>(thi, tlo, p.tw_mask, p.tw_lo_bits, g32 * uint32_t(j + u * TPC));
+      for (int i = 0; i < PER; ++i) {
+        const int k = tid + i * G::T;
+        if (k < N) {
+          C v = cmul(tvhi[i], tvlo[i]);
+          if (twinv) v = conj(v);
+          if constexpr (sizeof(C) == 8) reinterpret_cast<float4*>(tvs)[k] = make_float4(v.x, v.y, -v.y, v.x);
+          else tvs[k] = v;
+        }
+      }
+      if (t + gs < ntiles) tv_prefetch(t + gs);
     }
     // ---- stage 0 from the landing buffer (natural row order)
     const int sidx = it % G::NBUF;
-    C* buf = bufs + sidx * (G::BUF / sizeof(C));
+    C* buf = stage_buf(sidx);
     mbar_wait(&bars[sidx], uint32_t((it / G::NBUF) & 1));
     C a[E];
 #pragma unroll
     for (int u = 0; u < E / R0; ++u)
 #pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        C v = buf[(j + u * TPC + r * (N / R0)) * CT + cs];
-        v.y *= sx;
-        a[u * R0 + r] = v;
-      }
+      for (int r = 0; r < R0; ++r) a[u * R0 + r] = buf[(j + u * TPC + r * (N / R0)) * CT + cs];
+    if (sx < R(0)) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
+    }
     fft_stages<C, N, E, CT, false, 0, LAY, N, true>(a, buf, j, cs, tws);
     if constexpr (MID) {
       constexpr int RF = st_radix(N, E, NST - 1, false);
-      const C* mid = (const C*)p.mid + goff * p.mid_gmul;
+      // the tile's spectrum slice landed in shared memory with the data
+      if constexpr (sizeof(C) == 8) {
+        // quad spectrum: conj(a*s) = conj(cmul_q(a, q)); conj(a*conj s) = cmul_q(conj a, q)
+        const float4* mq = reinterpret_cast<const float4*>(stage_spec(sidx));
+        const bool mc = (f & F_MIDCONJ) != 0;
 #pragma unroll
-      for (int u = 0; u < E / RF; ++u)
+        for (int u = 0; u < E / RF; ++u)
 #pragma unroll
-        for (int r = 0; r < RF; ++r) {
-          const int k = j + u * TPC + r * (N / RF);
-          C sv = __ldg(&mid[k * p.mid_stride]);
-          sv.y *= smid;
-          a[u * RF + r] = conj(cmul(a[u * RF + r], sv));
-        }
+          for (int r = 0; r < RF; ++r) {
+            const int k = j + u * TPC + r * (N / RF);
+            const float4 q = mq[k];
+            C v = a[u * RF + r];
+            a[u * RF + r] = mc ? cmul_q(conj(v), q) : conj(cmul_q(v, q));
+          }
+      } else {
+        const C* mid = reinterpret_cast<const C*>(stage_spec(sidx));
+#pragma unroll
+        for (int u = 0; u < E / RF; ++u)
+#pragma unroll
+          for (int r = 0; r < RF; ++r) {
+            const int k = j + u * TPC + r * (N / RF);
+            C sv = mid[k];
+            sv.y *= smid;
+            a[u * RF + r] = conj(cmul(a[u * RF + r], sv));
+          }
+      }
       fft_stages<C, N, E, CT, true, 0, LAY, N, true>(a, buf, j, cs, tws);
     }
-    // ---- the landing buffer is free: start the load NBUF tiles ahead
+    // all exchange reads of the landing buffer are done after this barrier
     __syncthreads();
-    if (tid == 0 && t + G::NBUF * int(gridDim.x) < ntiles) {
-      fence_proxy_async();
-      issue(t + G::NBUF * gridDim.x, sidx);
+    if constexpr (!TS) {
+      // the landing buffer is free: start the load NBUF tiles ahead
+      if (tid == 0 && t + G::NBUF * gs < ntiles) {
+        fence_proxy_async();
+        issue(t + G::NBUF * gs, sidx);
+      }
     }
-    // ---- epilogue straight from registers
+    // ---- epilogue: four-step twiddle, conj/scale, then either direct stores
+    //      (TS = false) or a staged tile written back by one TMA store
     C* yc = (C*)p.y + yb;
 #pragma unroll
     for (int u = 0; u < E / RL; ++u) {
       const int bb = j + u * TPC;
       C* au = a + u * RL;
       if constexpr (TW) {
-        if (pre_conj != twinv) {
 #pragma unroll
-          for (int r = 0; r < RL; ++r) au[r] = conj(au[r]);
-        }
-        au[0] = cmul(au[0], wbase[u]);
-        apply_powers<RL>(au, wp);
-#pragma unroll
-        for (int r = 1; r < RL; ++r) au[r] = cmul(au[r], wbase[u]);
-        if (twinv) {
-#pragma unroll
-          for (int r = 0; r < RL; ++r) au[r] = conj(au[r]);
+        for (int r = 0; r < RL; ++r) {
+          const C v = pre_conj ? conj(au[r]) : au[r];
+          au[r] = tw_mul<true>(v, tvs, bb + r * (N / RL));
         }
       }
       C* yk = yc + int64_t(bb) * p.ysi;
+      if (s_re != R(1) || s_im != R(1)) {
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          au[r].x *= s_re;
+          au[r].y *= s_im;
+        }
+      }
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        C v = au[r];
-        v.x *= s_re;
-        v.y *= s_im;
-        yk[int64_t(r * (N / RL)) * p.ysi] = v;
+        if constexpr (TS) buf[(bb + r * (N / RL)) * CT + cs] = au[r];
+        else yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
       }
     }
+    if constexpr (!TS && TW) __syncthreads();  // tile twiddles are rebuilt next
+    if constexpr (TS) {
+      fence_proxy_async();  // this thread's tile writes -> visible to the TMA engine
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t q1, q2, c0;
+        decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, q1, q2, c0);
+        tma_store_5d(&ymap, buf, int(c0 * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
+        bulk_commit();
+        if (t + G::NBUF * gs < ntiles) {
+          bulk_wait_read0();  // the store has read the buffer: refill it
+          issue(t + G::NBUF * gs, sidx);
+        }
+      }
+    }
+  }
+  if constexpr (TS) {
+    if (tid == 0) bulk_wait0();
   }
 }
 
 // Launch when the pass qualifies (complex in/out, no masks, TMA-compatible
 // view); returns false so the caller falls back to the per-tile kernel.
-template <class C, int N>
-inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
-  using G = TmaGeom<C, N>;
+inline bool tma_store_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMAT_NO_TMA_STORE");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <class C, int N, int EP, int NB>
+inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
+  using G = TmaGeom<C, N, EP, NB>;
   if (a.x_real || a.y_real || a.pre || a.post || a.accumulate) return false;
   if (a.inner % G::CT != 0) return false;
+  // per-tile shared four-step twiddles / spectrum slices need goff uniform
+  // across a tile, and the slice must be contiguous
+  if ((a.tw_on || a.mid) && a.g_mod > 1 && (a.g_div % G::CT) != 0) return false;
+  if (a.mid && a.mid_stride != 1) return false;
   const FftDev d = make_fft_dev(a, N);
   if (d.flags & (F_PAD | F_TRUNC)) return false;
   const int64_t n1 = a.nb / (a.n2 * a.inner);
-  CUtensorMap map;
+  CUtensorMap map, ymap;
   if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT)) return false;
+  // TMA-store epilogue when the output view is TMA-compatible as well
+  const bool ts = tma_store_enabled() &&
+                  make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT);
+  if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int64_t slots = int64_t(num_sms(dev)) * G::MINB;
-  const int grid = int(ntiles < slots ? ntiles : slots);
-  auto kern = fft_tma_kernel<C, N, false, false>;
-  if (a.mid && a.tw_on) kern = fft_tma_kernel<C, N, true, true>;
-  else if (a.mid) kern = fft_tma_kernel<C, N, true, false>;
-  else if (a.tw_on) kern = fft_tma_kernel<C, N, false, true>;
-  set_smem(kern, G::SMEM);
-  kern<<<grid, G::T, G::SMEM, s>>>(map, d, int(ntiles));
+  auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag) {
+    constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value;
+    using GV = TmaGeom<C, N, EP, NB, TV, MV>;
+    const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
+    const int grid = int(ntiles < slots ? ntiles : slots);
+    auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV>;
+    set_smem(kern, GV::SMEM);
+    kern<<<grid, GV::T, GV::SMEM, s>>>(map, ymap, d, int(ntiles));
+  };
+  auto pick2 = [&](auto ts_tag) {
+    if (a.mid && a.tw_on) pick(ts_tag, std::true_type{}, std::true_type{});
+    else if (a.mid) pick(ts_tag, std::true_type{}, std::false_type{});
+    else if (a.tw_on) pick(ts_tag, std::false_type{}, std::true_type{});
+    else pick(ts_tag, std::false_type{}, std::false_type{});
+  };
+  if (ts) pick2(std::true_type{});
+  else pick2(std::false_type{});
   SMAT_CUDA(cudaGetLastError());
   return true;
+}
+
+inline int tma_variant() {
+  static int v = -1;
+  if (v < 0) {
+    // 1 (default): radix-32 stages, 3-deep landing ring, one CTA per SM
+    // 2: radix-32, single buffer, two CTAs per SM;  3: radix-16 stages
+    const char* e = getenv("SMAT_TMA_VARIANT");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+template <class C, int N>
+inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
+  if constexpr (N >= 1024 && sizeof(C) == 8) {
+    const int v = tma_variant();
+    if (v == 1 || v == 0) return fft_tma_launch_v<C, N, 32, 3>(a, s);
+    if (v == 2) return fft_tma_launch_v<C, N, 32, 1>(a, s);
+  }
+  return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }
 
 }  // namespace smat
