@@ -33,9 +33,12 @@ from .errors import DimensionMismatch, MaterializationTooLarge
 
 DEFAULT_DENSE_CAP_BYTES = 2 ** 31  # 2 GiB materialization guard (core.py:16)
 
-# Host inputs are streamed through the device in column chunks of about this
-# many bytes so that H2D copies, device passes and D2H copies overlap.
-HOST_CHUNK_BYTES = 64 << 20
+# Host inputs whose (rows x K) block exceeds this many bytes are streamed
+# through the device in column chunks (H2D copies, device passes and D2H
+# copies of different chunks overlap on three streams); smaller blocks move as
+# one contiguous DMA each way, which is what saturates the host link — a
+# column chunk of a row-major block is a pitched copy of short rows.
+HOST_CHUNK_BYTES = 8 << 30
 
 
 class ScalarField(enum.Enum):

@@ -224,8 +224,11 @@ int smat_apply_host(const smat_plan* plan_c, int32_t direction, const void* x_ho
       const int s = int(k % S);
       const int64_t c0 = k * cc, w = std::min<int64_t>(cc, ncols - c0);
       cudaStream_t st = plan->streams[s];
-      SMAT_CUDA(cudaMemcpy2DAsync(plan->dx[s], size_t(w) * ex, (const char*)x_host + size_t(c0) * ex,
-                                  size_t(ncols) * ex, size_t(w) * ex, size_t(nin), cudaMemcpyHostToDevice, st));
+      if (w == ncols)  // whole block: one contiguous DMA at full link bandwidth
+        SMAT_CUDA(cudaMemcpyAsync(plan->dx[s], x_host, size_t(nin) * ncols * ex, cudaMemcpyHostToDevice, st));
+      else  // column chunk of a row-major block: pitched copy
+        SMAT_CUDA(cudaMemcpy2DAsync(plan->dx[s], size_t(w) * ex, (const char*)x_host + size_t(c0) * ex,
+                                    size_t(ncols) * ex, size_t(w) * ex, size_t(nin), cudaMemcpyHostToDevice, st));
       smat::Ctx c;
       c.device = p.device;
       c.dt = p.dt;
@@ -233,8 +236,11 @@ int smat_apply_host(const smat_plan* plan_c, int32_t direction, const void* x_ho
       c.ws = (char*)plan->dw[s];
       c.ws_size = plan->bw;
       smat::run_plan(p, c, direction, plan->dx[s], x_dtype, plan->dy[s], w);
-      SMAT_CUDA(cudaMemcpy2DAsync((char*)y_host + size_t(c0) * ey, size_t(ncols) * ey, plan->dy[s],
-                                  size_t(w) * ey, size_t(w) * ey, size_t(nout), cudaMemcpyDeviceToHost, st));
+      if (w == ncols)
+        SMAT_CUDA(cudaMemcpyAsync(y_host, plan->dy[s], size_t(nout) * ncols * ey, cudaMemcpyDeviceToHost, st));
+      else
+        SMAT_CUDA(cudaMemcpy2DAsync((char*)y_host + size_t(c0) * ey, size_t(ncols) * ey, plan->dy[s],
+                                    size_t(w) * ey, size_t(w) * ey, size_t(nout), cudaMemcpyDeviceToHost, st));
     }
     for (int i = 0; i < S; ++i) SMAT_CUDA(cudaStreamSynchronize(plan->streams[i]));
   });

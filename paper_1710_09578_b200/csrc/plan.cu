@@ -112,6 +112,18 @@ __global__ void fourstep_perm_kernel(const double2* a, double2* b, int64_t N1, i
   }
 }
 
+// S -> (S[2k], S[2k+1]) and the twiddles W_L^i (i < L/2) of the pruned
+// Toeplitz embedding.
+__global__ void split_even_odd_kernel(const double2* s, double2* se, double2* so, double2* tw, int64_t L) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < L / 2; k += int64_t(gridDim.x) * blockDim.x) {
+    se[k] = s[2 * k];
+    so[k] = s[2 * k + 1];
+    double sn, cs;
+    sincospi(-2.0 * double(k) / double(L), &sn, &cs);
+    tw[k] = make_double2(cs, sn);
+  }
+}
+
 __global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const float c = float(a[i].x), s = float(a[i].y);
@@ -532,13 +544,18 @@ struct FourierNode : Node {
   }
 };
 
+static bool pack_real_pairs(Blk& x, Blk& y, Geo& g, int plan_dt);
+
 // Circulant(c) (leaves.py:207-234): IFFT(spec * FFT(x)); backward uses conj(spec).
 struct CirculantNode : Node {
   int64_t n = 0;
   DevBuf* spec = nullptr;
   std::string describe() const override { return "Circulant(" + std::to_string(n) + ")"; }
   bool accepts_real() const override { return true; }
-  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y0, const Geo& g0, bool acc) override {
+    Blk x = x0, y = y0;
+    Geo g = g0;
+    pack_real_pairs(x, y, g, c.dt);
     XformIO io;
     io.x = x; io.x_rows = n; io.y = y; io.y_rows = n; io.acc = acc;
     io.mid = spec->p; io.mid_conj = adj;
@@ -548,21 +565,59 @@ struct CirculantNode : Node {
 };
 
 // Toeplitz(col, row_rest) (leaves.py:237-290): circulant embedding of length L.
+// Real operator on real data: two real columns (2c, 2c+1) of a (rows, K)
+// block are one complex column of the same memory viewed as (rows, K/2)
+// complex, and T(a + ib) = Ta + i Tb for real T — one complex transform does
+// two real columns and the result lands interleaved exactly where the two
+// real outputs belong.
+static bool pack_real_pairs(Blk& x, Blk& y, Geo& g, int plan_dt) {
+  if (dt_complex(plan_dt) || dt_complex(x.dt) || dt_complex(y.dt) || g.inner % 2) return false;
+  auto even = [](int64_t v) { return v % 2 == 0; };
+  if (!even(x.s1) || !even(x.s2) || !even(x.si) || !even(y.s1) || !even(y.s2) || !even(y.si)) return false;
+  x.dt = y.dt = dt_complex_of(plan_dt);
+  x.s1 /= 2; x.s2 /= 2; x.si /= 2;
+  y.s1 /= 2; y.s2 /= 2; y.si /= 2;
+  g.inner /= 2;
+  return true;
+}
+
 struct ToeplitzNode : Node {
   int64_t L = 0;
   DevBuf* spec = nullptr;
+  // pruned embedding (max(rows, cols) <= L/2): FFT_L of a half-zero input is
+  // the two half-length FFTs of x and W_L^i x, and only the first half of
+  // the inverse is kept — two length-L/2 convolutions instead of one of L
+  DevBuf* spec_e = nullptr;  // S[2k]
+  DevBuf* spec_o = nullptr;  // S[2k + 1]
+  DevBuf* twid = nullptr;    // W_L^i, i < L/2
   std::string describe() const override {
-    return "Toeplitz(" + std::to_string(rows) + "x" + std::to_string(cols) + ", L=" + std::to_string(L) + ")";
+    return "Toeplitz(" + std::to_string(rows) + "x" + std::to_string(cols) + ", L=" + std::to_string(L) +
+           (spec_e ? ", pruned halves" : "") + ")";
   }
   bool accepts_real() const override { return true; }
-  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y0, const Geo& g0, bool acc) override {
+    Blk x = x0, y = y0;
+    Geo g = g0;
+    pack_real_pairs(x, y, g, c.dt);
     XformIO io;
     io.x = x; io.x_rows = adj ? rows : cols;
     io.y = y; io.y_rows = adj ? cols : rows;
     io.acc = acc;
-    io.mid = spec->p; io.mid_conj = adj;
+    io.mid_conj = adj;
     io.scale = 1.0 / double(L);
-    run_xform(c, L, g, io);
+    if (!spec_e) {
+      io.mid = spec->p;
+      run_xform(c, L, g, io);
+      return;
+    }
+    io.mid = spec_e->p;
+    run_xform(c, L / 2, g, io);
+    io.mid = spec_o->p;
+    io.pre = twid->p;
+    io.post = twid->p;
+    io.post_conj = true;
+    io.acc = true;
+    run_xform(c, L / 2, g, io);
   }
 };
 
@@ -1031,6 +1086,18 @@ struct Builder {
         DevBuf* sp = new_buf(p, SMAT_C128, t->L);
         device_fft_c128(p, t->L, eb->p, sp->p);
         t->spec = spectrum_for_plan(p, sp, cdt);
+        if (t->L > kTileMax && t->L / 2 <= kTileMax && std::max(n, m) <= t->L / 2) {
+          const int64_t h = t->L / 2;
+          DevBuf* se = new_buf(p, SMAT_C128, h);
+          DevBuf* so = new_buf(p, SMAT_C128, h);
+          DevBuf* tw = new_buf(p, SMAT_C128, h);
+          split_even_odd_kernel<<<256, 256>>>((const double2*)sp->p, (double2*)se->p, (double2*)so->p,
+                                              (double2*)tw->p, t->L);
+          SMAT_CUDA(cudaGetLastError());
+          t->spec_e = spectrum_for_plan(p, se, cdt);
+          t->spec_o = spectrum_for_plan(p, so, cdt);
+          t->twid = narrow_c128(p, tw, cdt);
+        }
         out = t;
         break;
       }

@@ -1,0 +1,126 @@
+"""Full-size parity of the five BASELINE.json configurations on the device.
+
+Each configuration runs forward and backward over its whole (rows, K) block
+on the GPU; the CPU oracle (numpy restatement of the reference algorithm,
+pinned to the reference in tests/test_oracle.py) checks a sample of columns —
+bit-exact for the integer and float64 Walsh-Hadamard transform, relative L2
+<= 1e-5 (complex64/float32) and <= 1e-12 (complex128) per column — and
+size-independent properties check the whole block: the adjoint identity
+<A x, y> = <x, A^H y>, linearity, and transform round trips.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1710_09578_b200 as sm
+from conftest import max_col_rel_l2
+from oracle import linop_oracle as orc
+from paper_1710_09578_b200 import configs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _cuda(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _adjoint_gap(op, x, y):
+    """|<Ax, y> - <x, A^H y>| / (|Ax| |y|) over the whole block (float64 sums)."""
+    import torch
+
+    ax = op.forward(x).to(torch.complex128)
+    ahy = op.backward(y).to(torch.complex128)
+    xx = x.to(torch.complex128)
+    yy = y.to(torch.complex128)
+    lhs = torch.sum(torch.conj(yy) * ax)
+    rhs = torch.sum(torch.conj(ahy) * xx)
+    return float(abs(lhs - rhs) / (torch.linalg.norm(ax) * torch.linalg.norm(yy)))
+
+
+def test_c1_full_exact():
+    w = configs.make(1)
+    op = configs.operator(1, w)
+    o = orc.hadamard(10)
+    assert np.array_equal(op.forward(w.X), orc.apply(o, w.X))
+    assert np.array_equal(op.backward(w.X), orc.apply(o, w.X, 1))
+    yi = op.forward(w.extra["Xi"])
+    assert yi.dtype == np.int32
+    assert np.array_equal(yi.astype(np.int64), orc.apply(o, w.extra["Xi"]).astype(np.int64))
+
+
+def test_c2_circulant_full():
+    w = configs.make(2)
+    op = configs.operator(2, w)
+    oc = orc.circulant(w.params["c"])
+    X = _cuda(w.X)
+    Y = op.forward(X)
+    Z = op.backward(X)
+    cols = [0, 37, 63]
+    xs = w.X[:, cols]
+    assert max_col_rel_l2(Y.cpu().numpy()[:, cols], orc.apply(oc, xs, 0)) <= 1e-5
+    assert max_col_rel_l2(Z.cpu().numpy()[:, cols], orc.apply(oc, xs, 1)) <= 1e-5
+    # whole block: adjoint identity and linearity
+    assert _adjoint_gap(op, X, Z) <= 1e-5
+    lin = op.forward(2 * X[:, :8] - 3j * X[:, 8:16])
+    assert max_col_rel_l2((lin).cpu().numpy(), (2 * Y[:, :8] - 3j * Y[:, 8:16]).cpu().numpy()) <= 1e-5
+
+
+def test_c3_toeplitz_full():
+    import torch
+
+    w = configs.make(3)
+    op = configs.operator(3, w)
+    p = w.params
+    ot = orc.toeplitz(p["col"], p["row_rest"])
+    X = _cuda(w.X)
+    Y = op.forward(X)
+    Z = op.backward(X)
+    assert Y.dtype == torch.float32 and Y.shape == (3000, 4096)
+    cols = list(range(0, 4096, 64))
+    assert max_col_rel_l2(Y.cpu().numpy()[:, cols], orc.apply(ot, w.X[:, cols], 0)) <= 1e-5
+    assert max_col_rel_l2(Z.cpu().numpy()[:, cols], orc.apply(ot, w.X[:, cols], 1)) <= 1e-5
+    # all 4096 columns against a float64 dense product on the device
+    n = 3000
+    col = torch.from_numpy(p["col"].astype(np.float64))
+    row = torch.from_numpy(np.concatenate([[p["col"][0]], p["row_rest"]]).astype(np.float64))
+    i = torch.arange(n)
+    d = i[:, None] - i[None, :]
+    T = torch.where(d >= 0, col[d.clamp(min=0)], row[(-d).clamp(min=0)]).cuda()
+    ref = T @ X.double()
+    err = torch.linalg.norm(Y.double() - ref, dim=0) / torch.linalg.norm(ref, dim=0)
+    assert float(err.max()) <= 1e-5
+    refb = T.T @ X.double()
+    errb = torch.linalg.norm(Z.double() - refb, dim=0) / torch.linalg.norm(refb, dim=0)
+    assert float(errb.max()) <= 1e-5
+
+
+def test_c4_kron_full():
+    w = configs.make(4)
+    op = configs.operator(4, w)
+    p = w.params
+    ok = orc.kron(orc.hadamard(6), orc.fourier(128), orc.circulant(p["c"]))
+    X = _cuda(w.X)
+    Y = op.forward(X)
+    Z = op.backward(X)
+    cols = [0, 31]
+    assert max_col_rel_l2(Y.cpu().numpy()[:, cols], orc.apply(ok, w.X[:, cols], 0)) <= 1e-5
+    assert max_col_rel_l2(Z.cpu().numpy()[:, cols], orc.apply(ok, w.X[:, cols], 1)) <= 1e-5
+    assert _adjoint_gap(op, X, Z) <= 1e-5
+
+
+def test_c5_chain_full():
+    w = configs.make(5)
+    op = configs.operator(5, w)
+    p = w.params
+    o5 = orc.chain_c5(p["N"], p["d1"], p["d2"], p["U"], p["V"])
+    X = _cuda(w.X)
+    Y = op.forward(X)
+    Z = op.backward(X)
+    cols = [0, 127]
+    assert max_col_rel_l2(Y.cpu().numpy()[:, cols], orc.apply(o5, w.X[:, cols], 0)) <= 1e-12
+    assert max_col_rel_l2(Z.cpu().numpy()[:, cols], orc.apply(o5, w.X[:, cols], 1)) <= 1e-12
+    assert _adjoint_gap(op, X, Z) <= 1e-12
