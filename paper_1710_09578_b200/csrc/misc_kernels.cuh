@@ -61,4 +61,22 @@ struct GemmArgs {
 // Returns the number of kernels launched (counted only when dry).
 int launch_gemm(int dt, const GemmArgs& a, int device, cudaStream_t s, bool dry);
 
+// Rank-r (r <= 32) factor kernels of LowRank = U diag(s) V^H on row-contiguous
+// (rows, K) blocks (reference vehicle: Product(Dense(U), Dense(V^H)),
+// leaves.py:40-46):
+//   contract: W (r x K) = F^H X            (F = V forward, U backward; W zeroed first)
+//   expand:   Y (=|+=) G diag(s) W          (G = U forward, V backward)
+struct LowRankArgs {
+  const void* F = nullptr;  // (rows x r) row-major
+  const void* x = nullptr;  // (rows x K), row stride ldx
+  void* w = nullptr;        // (r x K) contiguous
+  void* y = nullptr;        // (rows x K), row stride ldy
+  const void* s = nullptr;  // r or null
+  int32_t s_conj = 0, accumulate = 0;
+  int64_t rows = 0, r = 0, K = 0, ldx = 0, ldy = 0;
+};
+// number of launches (dry) or launch
+int launch_lowrank_contract(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry);
+int launch_lowrank_expand(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry);
+
 }  // namespace smat

@@ -124,6 +124,12 @@ __global__ void split_even_odd_kernel(const double2* s, double2* se, double2* so
   }
 }
 
+template <class C>
+__global__ void vec_mul_kernel(const C* a, const C* b, C* o, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    o[i] = cmul(a[i], b[i]);
+}
+
 __global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const float c = float(a[i].x), s = float(a[i].y);
@@ -360,6 +366,10 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
 }
 
 // ==================================================== FWHT engine =========
+// One FWHT pass over bits [lo, lo+w) of a 2^order transform.  x_rows /
+// y_rows mask the global row r = l + 2^lo*m + 2^(lo+w)*h: zero-pad rows
+// r >= x_rows on load (first pass only, lo == 0) and skip rows r >= y_rows on
+// store (last pass only, lo + w == order) — Partial(Hadamard, arange, arange).
 static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& x, const Blk& y,
                      bool acc, int64_t x_rows, int64_t y_rows) {
   WhtArgs a;
@@ -376,11 +386,17 @@ static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& 
     a.inner = (int64_t(1) << lo) * g.inner;
     a.nb = g.n2 * hi_cnt * a.inner;
     a.g_div = g.inner;
-    a.g_mod = int64_t(1) << lo;
-    a.gin_stride = a.gout_stride = int64_t(1) << lo;
-    // global row = l + 2^lo * (m + 2^w * h): only the l part is in goff; the
-    // validity masks of multi-pass transforms are applied on the full rows, so
-    // they are only allowed on single-pass calls.
+    if (lo == 0) {  // first pass: r = m + 2^w * h, h = (b / ic) % hi
+      a.g_mod = hi_cnt;
+      a.g_mul = int64_t(1) << w;
+      a.gin_stride = a.gout_stride = 1;
+    } else {  // r = l + 2^lo * m (+ 2^(lo+w) h, only masked when hi == 1)
+      a.g_mod = int64_t(1) << lo;
+      a.g_mul = 1;
+      a.gin_stride = a.gout_stride = int64_t(1) << lo;
+    }
+    SMAT_CHECK(x_rows == INT64_MAX || lo == 0, SMAT_UNSUPPORTED, "fwht input mask on a middle pass");
+    SMAT_CHECK(y_rows == INT64_MAX || hi_cnt == 1, SMAT_UNSUPPORTED, "fwht output mask on a middle pass");
   }
   a.n_valid_in = x_rows;
   a.n_valid_out = y_rows;
@@ -388,18 +404,25 @@ static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& 
   c.wht(c.dt, 1 << w, a);
 }
 
-static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc) {
+// Hadamard of order `order` along the rows of x -> y; x has x_rows valid rows
+// (zero padding beyond), only the first y_rows rows of the result are written.
+static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_rows = INT64_MAX,
+                    int64_t y_rows = INT64_MAX) {
   const int64_t N = int64_t(1) << order;
+  if (x_rows >= N) x_rows = INT64_MAX;
+  if (y_rows >= N) y_rows = INT64_MAX;
   if (N == 1) {
     point_copy(c, x, y, g, 1, acc);
     return;
   }
   if (N <= kTileMax) {
-    wht_pass(c, order, 0, order, g, x, y, acc, INT64_MAX, INT64_MAX);
+    wht_pass(c, order, 0, order, g, x, y, acc, x_rows, y_rows);
     return;
   }
   if (!merge_outer(g, x, y)) {
-    for_each_o1(g, x, y, [&](const Geo& g1, const Blk& xo, const Blk& yo) { run_wht(c, order, g1, xo, yo, acc); });
+    for_each_o1(g, x, y, [&](const Geo& g1, const Blk& xo, const Blk& yo) {
+      run_wht(c, order, g1, xo, yo, acc, x_rows, y_rows);
+    });
     return;
   }
   SMAT_CHECK(x.si == g.inner, SMAT_UNSUPPORTED, "multi-pass FWHT needs row-contiguous input");
@@ -408,14 +431,15 @@ static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc) {
   for (int i = 0; i < order % npass; ++i) widths[i] += 1;
   const size_t m0 = c.mark();
   Blk T = y;
-  const bool y_ok = !acc && y.si == g.inner;
+  const bool y_ok = !acc && y.si == g.inner && y_rows == INT64_MAX;
   if (!y_ok) T = c.alloc_blk(c.dt, g, N);
   int lo = 0;
   for (int p = 0; p < npass; ++p) {
     const bool last = p == npass - 1;
     const Blk& src = p == 0 ? x : T;
     const Blk& dst = (last && !y_ok) ? y : T;
-    wht_pass(c, order, lo, widths[p], g, src, dst, last && !y_ok ? acc : false, INT64_MAX, INT64_MAX);
+    wht_pass(c, order, lo, widths[p], g, src, dst, last && !y_ok ? acc : false, p == 0 ? x_rows : INT64_MAX,
+             last ? y_rows : INT64_MAX);
     lo += widths[p];
   }
   c.release(m0);
@@ -488,6 +512,19 @@ struct LowRankNode : Node {
     DevBuf* first = adj ? U : V;   // contracted with x (conj-transposed)
     DevBuf* second = adj ? V : U;  // expands back
     const int64_t kin = adj ? rows : cols, kout = adj ? cols : rows;
+    if (dt_complex(c.dt) && r <= 32 && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner) {
+      // tall-skinny rank-r kernels: W = F^H x (row-slab reduction), y (+)= G diag(s) W
+      void* w = c.alloc(size_t(r) * size_t(g.inner) * dt_size(c.dt));
+      LowRankArgs la;
+      la.F = first->p; la.x = x.p; la.w = w; la.rows = kin; la.r = r; la.K = g.inner; la.ldx = x.si;
+      c.lr_contract(la);
+      LowRankArgs lb;
+      lb.F = second->p; lb.w = w; lb.y = y.p; lb.rows = kout; lb.r = r; lb.K = g.inner; lb.ldy = y.si;
+      lb.s = s ? s->p : nullptr; lb.s_conj = adj; lb.accumulate = acc;
+      c.lr_expand(lb);
+      c.release(m0);
+      return;
+    }
     Blk t = c.alloc_blk(c.dt, g, r);
     GemmArgs a;
     a.A = first->p; a.lda = r; a.adj = 1; a.m = r; a.k = kin;
@@ -541,6 +578,33 @@ struct FourierNode : Node {
     io.scale = 1.0 / double(M);
     io.conj_x = adj; io.conj_y = adj;  // F^H y = conj(F conj(y))
     run_xform(c, M, g, io);
+  }
+};
+
+// Diag(dl) · Fourier(n) · Diag(dr) as ONE transform: the diagonals fold into
+// the pre/post vectors of the FFT passes (for Bluestein, into the chirps:
+// pre = chirp*dr, post = chirp*dl), so the chain costs no pointwise pass.
+//   forward  y = dl * F(dr * x)
+//   adjoint  y = conj(dr) * F^H(conj(dl) * x) = conj(dr * F(dl * conj x))
+struct DiagFourierNode : Node {
+  FourierNode* F = nullptr;
+  DevBuf* vr = nullptr;  // applied before the transform (forward): chirp*dr or dr
+  DevBuf* vl = nullptr;  // applied after it: chirp*dl or dl (may be the bare chirp)
+  std::string describe() const override { return "DiagFourierDiag(" + F->describe() + ")"; }
+  bool accepts_real() const override { return true; }
+  void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
+    XformIO io;
+    io.x = x; io.x_rows = F->n; io.y = y; io.y_rows = F->n; io.acc = acc;
+    io.pre = (adj ? vl : vr) ? (adj ? vl : vr)->p : nullptr;
+    io.post = (adj ? vr : vl) ? (adj ? vr : vl)->p : nullptr;
+    io.conj_x = adj; io.conj_y = adj;
+    if (F->M) {
+      io.mid = F->kspec->p;
+      io.scale = 1.0 / double(F->M);
+      run_xform(c, F->M, g, io);
+    } else {
+      run_xform(c, F->n, g, io);
+    }
   }
 };
 
@@ -783,10 +847,21 @@ struct PartialNode : Node {
   DevBuf* ridx = nullptr;  // may be null (all rows)
   DevBuf* cidx = nullptr;
   bool r_unique = true, c_unique = true;
-  std::string describe() const override { return "Partial(" + base->describe() + ")"; }
+  // base is a Hadamard and both selections are prefixes arange(k): the
+  // "Hadamard-padded" operator — zero-pad on load / truncate on store of the
+  // FWHT passes, no scatter, gather or padded copies
+  int had_order = -1;
+  std::string describe() const override {
+    return std::string(had_order >= 0 ? "PaddedHadamard(" : "Partial(") + base->describe() + ")";
+  }
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
     const size_t m0 = c.mark();
     Blk x = promote(c, x0, g, adj ? rows : cols);
+    if (had_order >= 0) {
+      run_wht(c, had_order, g, x, y, acc, adj ? rows : cols, adj ? cols : rows);
+      c.release(m0);
+      return;
+    }
     DevBuf* in_idx = adj ? ridx : cidx;    // scatter side
     DevBuf* out_idx = adj ? cidx : ridx;   // gather side
     const bool in_unique = adj ? r_unique : c_unique;
@@ -970,6 +1045,44 @@ struct Builder {
     return r;
   }
 
+  // elementwise product of two plan-precision complex vectors (either may be null)
+  DevBuf* vec_product(DevBuf* a, DevBuf* b, int cdt) {
+    if (!a && !b) return nullptr;
+    if (!a || !b) return a ? a : b;
+    DevBuf* o = new_buf(p, cdt, a->len);
+    if (cdt == SMAT_C128)
+      vec_mul_kernel<double2><<<1184, 256>>>((const double2*)a->p, (const double2*)b->p, (double2*)o->p, a->len);
+    else
+      vec_mul_kernel<float2><<<1184, 256>>>((const float2*)a->p, (const float2*)b->p, (float2*)o->p, a->len);
+    SMAT_CUDA(cudaGetLastError());
+    return o;
+  }
+
+  // Product factor list: fold Diag · Fourier · Diag (and Diag · Fourier,
+  // Fourier · Diag) into one DiagFourierNode.
+  void fuse_diag_fourier(std::vector<Node*>& f) {
+    const int cdt = cplx_of(p.dt);
+    if (dt_int(p.dt) || !dt_complex(p.dt)) return;
+    for (size_t i = 0; i < f.size(); ++i) {
+      auto* F = dynamic_cast<FourierNode*>(f[i]);
+      if (!F) continue;
+      DiagNode* dl = i > 0 ? dynamic_cast<DiagNode*>(f[i - 1]) : nullptr;
+      DiagNode* dr = i + 1 < f.size() ? dynamic_cast<DiagNode*>(f[i + 1]) : nullptr;
+      if (!dl && !dr) continue;
+      auto* n = add<DiagFourierNode>();
+      n->F = F;
+      n->rows = F->rows;
+      n->cols = F->cols;
+      DevBuf* chirp = F->M ? F->chirp : nullptr;
+      n->vr = vec_product(chirp, dr ? dr->d : nullptr, cdt);
+      n->vl = vec_product(chirp, dl ? dl->d : nullptr, cdt);
+      const size_t lo = dl ? i - 1 : i, hi = dr ? i + 1 : i;
+      f.erase(f.begin() + lo, f.begin() + hi + 1);
+      f.insert(f.begin() + lo, n);
+      i = lo;
+    }
+  }
+
   std::vector<Node*> memo;  // shared sub-operators are compiled once
 
   Node* build(int idx) {
@@ -1113,7 +1226,8 @@ struct Builder {
         SMAT_CHECK(!a->f.empty(), SMAT_BAD_ARG, "empty product");
         for (size_t k = 0; k + 1 < a->f.size(); ++k)
           SMAT_CHECK(a->f[k]->cols == a->f[k + 1]->rows, SMAT_BAD_SHAPE, "product chain mismatch");
-        out = a;
+        fuse_diag_fourier(a->f);
+        out = a->f.size() == 1 ? a->f[0] : a;
         break;
       }
       case SMAT_SUM: {
@@ -1140,6 +1254,19 @@ struct Builder {
         if (nd.iparam[1]) {
           a->cidx = upload_param(p, nd.param[1], SMAT_I64);
           a->c_unique = nd.iparam[3] != 0;
+        }
+        {
+          auto is_prefix = [](const smat_param& prm) {
+            if (prm.dtype != SMAT_I64) return false;
+            const int64_t* v = (const int64_t*)prm.data;
+            for (int64_t i = 0; i < prm.len; ++i)
+              if (v[i] != i) return false;
+            return true;
+          };
+          const smat_node& bn = nodes[children[nd.first_child]];
+          if (bn.kind == SMAT_HADAMARD && (!nd.iparam[0] || is_prefix(nd.param[0])) &&
+              (!nd.iparam[1] || is_prefix(nd.param[1])))
+            a->had_order = int(bn.iparam[0]);
         }
         out = a;
         break;

@@ -112,6 +112,16 @@ struct Ctx {
     note("gemm");
     if (!measure) launch_gemm(dt, a, device, stream, false);
   }
+  void lr_contract(const LowRankArgs& a) {
+    launches += launch_lowrank_contract(dt, a, device, stream, true);
+    note("lowrank_contract");
+    if (!measure) launch_lowrank_contract(dt, a, device, stream, false);
+  }
+  void lr_expand(const LowRankArgs& a) {
+    launches += launch_lowrank_expand(dt, a, device, stream, true);
+    note("lowrank_expand");
+    if (!measure) launch_lowrank_expand(dt, a, device, stream, false);
+  }
 };
 
 // A device array owned by a plan.

@@ -93,6 +93,9 @@ struct WhtDev {
   FastDiv inner, n2;
   int32_t nb;
   int32_t acc;
+  // masks (MASK instantiation only)
+  FastDiv gdiv, gmod;
+  int32_t g_mul, gin_stride, gout_stride, n_valid_in, n_valid_out;
 };
 
 // b -> (o1, o2, c) with b = (o1*n2 + o2)*inner + c; returns the offset of the
@@ -290,7 +293,7 @@ __device__ __forceinline__ T zero_of() {
   else return T(0);
 }
 
-template <class T, int N>
+template <class T, int N, bool MASK>
 __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(const WhtDev p) {
   constexpr int E = tile_E(N);
   constexpr int CT = tile_CT(N, sizeof(T));
@@ -302,11 +305,16 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
   const uint32_t b = blockIdx.x * uint32_t(CT) + uint32_t(cs);
   const bool act = int32_t(b) < p.nb;
   int64_t xb = 0, yb = 0;
+  int32_t goff = 0;
   if (act) {
     uint32_t o1, o2, c;
     decode_batch(b, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c);
     xb = int64_t(o1) * p.xs1 + int64_t(o2) * p.xs2 + c;
     yb = int64_t(o1) * p.ys1 + int64_t(o2) * p.ys2 + c;
+    if constexpr (MASK) {
+      const uint32_t q = fdiv(b, p.gdiv.m, p.gdiv.s);
+      goff = int32_t(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d) * p.g_mul;
+    }
   }
   const T* x = (const T*)p.x + xb;
   T* y = (T*)p.y + yb;
@@ -316,7 +324,12 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
   for (int u = 0; u < E / R0; ++u) {
     const int bb = j + u * TPC;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) a[u * R0 + r] = act ? x[int64_t(bb * R0 + r) * p.xsi] : zero_of<T>();
+    for (int r = 0; r < R0; ++r) {
+      const int i = bb * R0 + r;
+      bool ok = act;
+      if constexpr (MASK) ok = ok && goff + i * p.gin_stride < p.n_valid_in;
+      a[u * R0 + r] = ok ? x[int64_t(i) * p.xsi] : zero_of<T>();
+    }
   }
   wht_stages<T, N, E, CT, 0>(a, sm, j, cs);
   constexpr int RL = st_radix(N, E, NST - 1, false);
@@ -328,7 +341,11 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
     const int base = (bb / NSL) * (NSL * RL) + (bb % NSL);
 #pragma unroll
     for (int r = 0; r < RL; ++r) {
-      const int64_t off = int64_t(base + r * NSL) * p.ysi;
+      const int k = base + r * NSL;
+      if constexpr (MASK) {
+        if (goff + k * p.gout_stride >= p.n_valid_out) continue;
+      }
+      const int64_t off = int64_t(k) * p.ysi;
       y[off] = p.acc ? y[off] + a[u * RL + r] : a[u * RL + r];
     }
   }
@@ -445,8 +462,6 @@ inline void wht_tile_launch(const WhtArgs& a, cudaStream_t s) {
   constexpr int CT = tile_CT(N, sizeof(T));
   SMAT_CHECK(a.nb < (int64_t(1) << 31) - 4096, SMAT_UNSUPPORTED, "fwht tile: batch count exceeds 2^31");
   SMAT_CHECK(fits31(a.xsi * N) && fits31(a.ysi * N), SMAT_UNSUPPORTED, "fwht tile: row stride too large");
-  SMAT_CHECK(a.n_valid_in >= N && a.n_valid_out >= N, SMAT_UNSUPPORTED,
-             "fwht tile: padding masks are not supported");
   WhtDev d{};
   d.x = a.x; d.y = a.y;
   d.xs1 = a.xs1; d.xs2 = a.xs2; d.ys1 = a.ys1; d.ys2 = a.ys2;
@@ -455,11 +470,28 @@ inline void wht_tile_launch(const WhtArgs& a, cudaStream_t s) {
   d.n2 = FastDiv(a.n2);
   d.nb = int32_t(a.nb);
   d.acc = a.accumulate;
+  const int64_t gmax_in = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gin_stride;
+  const int64_t gmax_out = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gout_stride;
+  const bool mask = gmax_in >= a.n_valid_in || gmax_out >= a.n_valid_out;
+  if (mask) {
+    SMAT_CHECK(fits31(gmax_in) && fits31(gmax_out), SMAT_UNSUPPORTED, "fwht tile: row index exceeds 2^31");
+    d.gdiv = FastDiv(a.g_div);
+    d.gmod = FastDiv(a.g_mod);
+    d.g_mul = int32_t(a.g_mul);
+    d.gin_stride = int32_t(a.gin_stride);
+    d.gout_stride = int32_t(a.gout_stride);
+    d.n_valid_in = int32_t(a.n_valid_in < INT32_MAX ? a.n_valid_in : INT32_MAX);
+    d.n_valid_out = int32_t(a.n_valid_out < INT32_MAX ? a.n_valid_out : INT32_MAX);
+  }
   const size_t smem = N > 1 ? size_t(sm_rows(N)) * CT * sizeof(T) : 0;
   const int64_t blocks = (a.nb + CT - 1) / CT;
   if (blocks == 0) return;
-  set_smem(wht_tile_kernel<T, N>, smem);
-  wht_tile_kernel<T, N><<<unsigned(blocks), tile_threads(N, sizeof(T)), smem, s>>>(d);
+  auto go = [&](auto kern) {
+    set_smem(kern, smem);
+    kern<<<unsigned(blocks), tile_threads(N, sizeof(T)), smem, s>>>(d);
+  };
+  if (mask) go(wht_tile_kernel<T, N, true>);
+  else go(wht_tile_kernel<T, N, false>);
   SMAT_CUDA(cudaGetLastError());
 }
 

@@ -47,7 +47,10 @@ struct WhtArgs {
   int64_t xs1 = 0, xs2 = 0, xsi = 0;
   int64_t ys1 = 0, ys2 = 0, ysi = 0;
   int64_t n2 = 1, inner = 1, nb = 0;
-  int64_t g_div = 1, g_mod = 1, gin_stride = 1, gout_stride = 1;
+  // global row g = ((b / g_div) % g_mod) * g_mul + i * g{in,out}_stride; rows
+  // with g >= n_valid_in load as zero, rows with g >= n_valid_out are not
+  // stored (the zero-pad / truncate of Partial(Hadamard, arange, arange))
+  int64_t g_div = 1, g_mod = 1, g_mul = 1, gin_stride = 1, gout_stride = 1;
   int64_t n_valid_in = INT64_MAX, n_valid_out = INT64_MAX;
   int32_t accumulate = 0;
 };
