@@ -237,17 +237,40 @@ def _peaks():
 
 
 def _pass_bytes(cfg: int, label: str, ncols: int) -> int | None:
-    """Algorithmic bytes of one launch of the labelled kernel (SURVEY.md §8d units)."""
+    """Algorithmic HBM bytes of one launch of the labelled pass (SURVEY.md §8d
+    units: each operand block read or written once, vectors once).  Labels are
+    smat_apply_profiled's: kernel_length[_spec][_tw|_twin][_msk]."""
+    K = ncols
+    if cfg == 1:
+        return 2 * 1024 * K * 8
     if cfg == 2:
         n = 1 << 20
-        return 2 * n * ncols * 8 + (n * 8 if label == "mid" else 0)
-    if cfg == 4:
-        return 2 * (1 << 21) * ncols * 8
-    if cfg == 1:
-        return 2 * 1024 * ncols * 8
+        return 2 * n * K * 8 + (n * 8 if "_spec" in label else 0)
     if cfg == 3:
-        return 2 * 3000 * ncols * 4
+        return None  # compute-bound (single tile pass per column pair), no HBM roofline
+    if cfg == 4:
+        return 2 * (1 << 21) * K * 8
+    if cfg == 5:
+        n = configs_c5_n()
+        M = 1 << (2 * n - 1).bit_length()
+        P = 1 << max(0, (n - 1).bit_length())
+        e = 16
+        if label.startswith("wht_"):
+            return (n + P) * K * e
+        if label == "lowrank_contract":
+            return n * K * e + n * 32 * e
+        if label == "lowrank_expand":
+            return n * 32 * e + 2 * n * K * e
+        if "_spec" in label:
+            return 2 * M * K * e + M * e
+        if label.startswith("fft_c128_"):  # Bluestein outer passes: n-row side, M-row side, chirp
+            return n * K * e + M * K * e + n * e
     return None
+
+
+def configs_c5_n():
+    from paper_1710_09578_b200 import configs
+    return configs.C5_N
 
 
 def _traffic(workload: str, kernel: str):
@@ -339,19 +362,39 @@ def run_native(args, cfg):
     for d, lab, t_ms in prof:
         by_kernel.setdefault(lab, []).append(t_ms)
     total = sum(sum(v) for v in by_kernel.values())
-    dom = max(by_kernel, key=lambda k: sum(by_kernel[k]))
-    dom_avg_ms = float(np.mean(by_kernel[dom]))
     peak, peak_src = _peaks()
+    # per-pass breakdown, and the roofline of the dominant kernel: the kernel
+    # family (precision + length, e.g. fft_c64_1024, all its fused variants)
+    # with the largest share of the step; achieved = its algorithmic bytes per
+    # launch over its mean launch time
+    passes = {}
+    for lab, ts in by_kernel.items():
+        pb = _pass_bytes(cfg, lab, K)
+        avg = float(np.mean(ts))
+        passes[lab] = {"launches_per_step": len(ts) / max(3, min(args.steps, 10)), "avg_ms": avg,
+                       "bytes_per_launch": pb, "GB/s": (pb / (avg / 1e3) / 1e9) if pb else None}
+
+    def family(lab):
+        parts = lab.split("_")
+        return "_".join(parts[:3]) if lab.startswith("fft_") else lab
+
+    fams = {}
+    for lab, ts in by_kernel.items():
+        fams.setdefault(family(lab), []).append(lab)
+    dom = max(fams, key=lambda f: sum(sum(by_kernel[l]) for l in fams[f]))
+    dom_t = sum(sum(by_kernel[l]) for l in fams[dom])
+    dom_n = sum(len(by_kernel[l]) for l in fams[dom])
     roofline = None
-    pb = _pass_bytes(cfg, "pass", K)
-    if pb is not None:
-        if cfg == 2:  # 3 launches per direction: 2 plain passes + the spectrum pass
-            pb = (3 * 2 * (1 << 20) * K * 8 + (1 << 20) * 8) / 3
+    if all(_pass_bytes(cfg, l, K) is not None for l in fams[dom]):
+        dom_b = sum(_pass_bytes(cfg, l, K) * len(by_kernel[l]) for l in fams[dom])
+        pb = dom_b / dom_n
+        dom_avg_ms = dom_t / dom_n
         achieved = pb / (dom_avg_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": _traffic(args.workload, dom),
+        roofline = {"bound": "hbm", "kernel": dom, "variants": sorted(fams[dom]), "achieved": achieved,
+                    "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": _traffic(args.workload, dom),
                     "bytes_per_launch": pb, "avg_launch_ms": dom_avg_ms,
-                    "share_of_step": sum(by_kernel[dom]) / total if total else None,
+                    "share_of_step": dom_t / total if total else None,
                     "peak_source": peak_src}
     alg = configs.algorithmic_bytes(cfg, K)
     transform_gbs = 2 * alg / (ms_step / 1e3) / 1e9
@@ -402,6 +445,7 @@ def run_native(args, cfg):
             "gpu_launches": int(args.steps * (launches[0] + launches[1])),
             "launches_per_step": {"forward": launches[0], "backward": launches[1]},
             "kernels_ms_per_step": {k: float(np.sum(v)) / max(3, min(args.steps, 10)) for k, v in by_kernel.items()},
+            "passes": passes,
             "plan": plan.describe(),
             "clocks": clk.summary(),
         }

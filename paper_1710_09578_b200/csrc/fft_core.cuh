@@ -25,8 +25,13 @@
 namespace smat {
 
 // ------------------------------------------------------ stage bookkeeping --
-// A length-N transform with E elements per thread runs stages of radix E
-// (forward list: E, E, ..., rem) or the mirrored list (rem, E, ..., E).
+// A length-N transform with E elements per thread runs stages of radix E and
+// at most one smaller remainder stage.  The FFT puts the remainder in the
+// middle when the E-stages split evenly around it (E^q/2, rem, E^q/2): the
+// list is then a palindrome, so the mirrored list the spectrum passes use for
+// their inverse transform is the same list and shares one staged twiddle
+// table.  Otherwise (and for the FWHT, whose stage order is fixed) the list is
+// linear (E, E, ..., rem); the mirrored list is its reverse.
 __host__ __device__ constexpr int st_count(int N, int E) {
   int s = 0, m = 1;
   while (m < N) {
@@ -35,13 +40,27 @@ __host__ __device__ constexpr int st_count(int N, int E) {
   }
   return s;
 }
-__host__ __device__ constexpr int st_radix_fwd(int N, int E, int s) {
+__host__ __device__ constexpr int st_radix_lin(int N, int E, int s) {
   int m = 1, r = 1;
   for (int i = 0; i <= s; ++i) {
     r = (N / m >= E ? E : N / m);
     m *= r;
   }
   return r;
+}
+__host__ __device__ constexpr int st_ns_lin(int N, int E, int s) {
+  int m = 1;
+  for (int i = 0; i < s; ++i) m *= st_radix_lin(N, E, i);
+  return m;
+}
+__host__ __device__ constexpr bool st_palindrome(int N, int E) {
+  return st_count(N, E) % 2 == 1 || st_radix_lin(N, E, st_count(N, E) - 1) == E;
+}
+__host__ __device__ constexpr int st_radix_fwd(int N, int E, int s) {
+  if (st_radix_lin(N, E, st_count(N, E) - 1) == E || st_count(N, E) % 2 == 0) return st_radix_lin(N, E, s);
+  // odd stage count with a remainder: move it to the middle
+  const int mid = st_count(N, E) / 2;
+  return s == mid ? st_radix_lin(N, E, st_count(N, E) - 1) : E;
 }
 __host__ __device__ constexpr int st_radix(int N, int E, int s, bool mirror) {
   return mirror ? st_radix_fwd(N, E, st_count(N, E) - 1 - s) : st_radix_fwd(N, E, s);
@@ -171,14 +190,30 @@ __device__ __forceinline__ double2 ld_spec(const double2* mid, int64_t i) { retu
 
 // Exchange-buffer row map.  LAY == 0: padded rows (row + row/16, the buffer
 // holds sm_rows(N) rows).  LAY = X > 0: dense rows permuted as
-// row ^ ((row >> 4) & (X - 1)) — X = rows per 128 bytes — so the radix-16
-// scatter (rows 16 apart) spreads over all bank groups without padding, which
-// lets a dense TMA landing buffer double as the exchange buffer.
-template <int LAY>
+// row ^ ((row >> SH) & (X - 1)) — X = rows per 128 bytes, SH = log2 of the
+// writing stage's radix — so the radix-R scatter (rows R apart) spreads over
+// all bank groups without padding, which lets a dense TMA landing buffer
+// double as the exchange buffer.
+template <int LAY, int SH = 4>
 __device__ __forceinline__ int ex_row(int row) {
   if constexpr (LAY == 0) return row + (row >> 4);
   else if constexpr (LAY == 1) return row;
-  else return row ^ ((row >> 4) & (LAY - 1));
+  else return row ^ ((row >> SH) & (LAY - 1));
+}
+
+// Staged twiddle table (shared-memory tables of the TMA pass): stage s with
+// stride NS > 1 and radix R reads W_N^(r*k*N/(NS*R)) at
+// st_twoff(s) + k*(R-1) + r-1 — consecutive butterflies k sit (R-1) entries
+// apart, an odd stride, so a warp's lookups are bank-conflict free.  The
+// table holds N - R0 entries.
+__host__ __device__ constexpr int st_twoff(int N, int E, int s, bool mirror) {
+  int off = 0, ns = 1;
+  for (int i = 0; i < s; ++i) {
+    const int r = st_radix(N, E, i, mirror);
+    if (ns > 1) off += ns * (r - 1);
+    ns *= r;
+  }
+  return off;
 }
 
 // ------------------------------------------------- block FFT (Stockham) ----
@@ -192,14 +227,22 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
     constexpr int R = st_radix(N, E, S, MIR);
     constexpr int NS = st_ns(N, E, S, MIR);
     constexpr int TPC = N / E;
+    constexpr int SH = log2_c(R);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       if constexpr (NS > 1) {
         const int k = (j + u * TPC) & (NS - 1);
-        constexpr int step = TWN / (NS * R);
-        const int ks = k * step;
+        if constexpr (TWS) {
+          // staged shared table (see st_twoff)
+          const int t0 = st_twoff(N, E, S, MIR) + k * (R - 1) - 1;
 #pragma unroll
-        for (int r = 1; r < R; ++r) a[u * R + r] = tw_mul<TWS>(a[u * R + r], tw, r * ks);
+          for (int r = 1; r < R; ++r) a[u * R + r] = tw_mul<true>(a[u * R + r], tw, t0 + r);
+        } else {
+          constexpr int step = TWN / (NS * R);
+          const int ks = k * step;
+#pragma unroll
+          for (int r = 1; r < R; ++r) a[u * R + r] = tw_mul<false>(a[u * R + r], tw, r * ks);
+        }
       }
       dft_small<R>(a + u * R);
     }
@@ -212,14 +255,14 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
         const int k = bb & (NS - 1);
         const int base = (bb - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[ex_row<LAY>(base + r * NS) * CT + cs] = a[u * R + r];
+        for (int r = 0; r < R; ++r) sm[ex_row<LAY, SH>(base + r * NS) * CT + cs] = a[u * R + r];
       }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < E / R2; ++u) {
         const int bb = j + u * TPC;
 #pragma unroll
-        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[ex_row<LAY>(bb + r * (N / R2)) * CT + cs];
+        for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[ex_row<LAY, SH>(bb + r * (N / R2)) * CT + cs];
       }
       fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS>(a, sm, j, cs, tw);
     }
@@ -231,13 +274,13 @@ template <class T, int N, int E, int CT, int S>
 __device__ __forceinline__ void wht_stages(T* a, T* sm, int j, int cs) {
   constexpr int NST = st_count(N, E);
   if constexpr (S < NST) {
-    constexpr int R = st_radix(N, E, S, false);
+    constexpr int R = st_radix_lin(N, E, S);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) wht_small<R>(a + u * R);
     if constexpr (S + 1 < NST) {
-      constexpr int NS = st_ns(N, E, S, false);
-      constexpr int R2 = st_radix(N, E, S + 1, false);
-      constexpr int NS2 = st_ns(N, E, S + 1, false);
+      constexpr int NS = st_ns_lin(N, E, S);
+      constexpr int R2 = st_radix_lin(N, E, S + 1);
+      constexpr int NS2 = st_ns_lin(N, E, S + 1);
       constexpr int TPC = N / E;
       __syncthreads();
 #pragma unroll

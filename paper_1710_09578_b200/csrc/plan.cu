@@ -255,6 +255,16 @@ static void xform_pass_common(FftArgs& a, Ctx& c) {
   a.tw = twiddle4096(c.device, cplx_of(c.dt) == SMAT_C128);
 }
 
+static bool tw_in_pass3(bool dbl, int64_t N1) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("SMAT_TW_PASS3");
+    force = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  if (force >= 0) return force == 1;
+  return dbl && N1 >= 2048;
+}
+
 static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   const int cdt = cplx_of(c.dt);
   const bool dbl = cdt == SMAT_C128;
@@ -330,6 +340,10 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.scale = io.scale; a.accumulate = io.acc;
     c.fft(cdt, int(N1), a);
   } else {
+    // The inverse four-step twiddle sits between pass 2's IFFT and pass 3; it
+    // goes to pass 3's input when pass 2's tile has no shared memory left for
+    // it (double precision, N1 >= 2048) or when forced by SMAT_TW_PASS3=0/1.
+    const bool tw3 = tw_in_pass3(dbl, N1);
     // ---- pass 2 (convolution): W -> W
     {
       FftArgs a;
@@ -342,7 +356,9 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       // spectra longer than one tile are stored in four-step order
       // (spec_fs[k2*N1 + k1] = spec[k2 + N2*k1], see spectrum_for_plan)
       a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = 1; a.mid_gmul = N1;
-      a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+      if (!tw3) {
+        a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+      }
       c.fft(cdt, int(N1), a);
     }
     // ---- pass 3: W -> y
@@ -357,6 +373,11 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.g_div = ic; a.g_mod = N1; a.gout_stride = N1;
       a.n_valid_out = io.y_rows;
       a.inv = 1;
+      if (tw3) {
+        // pass 2's inverse twiddle W^-(n1*k2), applied to this pass's input
+        a.tw_on = 1; a.tw_pre = 1; a.tw_inv = 1;
+        a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+      }
       a.post = io.post; a.post_conj = io.post_conj; a.conj_y = io.conj_y;
       a.scale = io.scale; a.accumulate = io.acc;
       c.fft(cdt, int(N2), a);

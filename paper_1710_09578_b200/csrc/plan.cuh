@@ -84,7 +84,17 @@ struct Ctx {
   // counted launches (skipped in measure mode)
   void fft(int cdt, int N, const FftArgs& a) {
     ++launches;
-    note(std::string(cdt == SMAT_C128 ? "fft_c128_" : "fft_c64_") + std::to_string(N));
+    // label: precision, length and the fused extras (spectrum, four-step
+    // twiddle, pad/truncate/pre/post masks)
+    std::string lab = std::string(cdt == SMAT_C128 ? "fft_c128_" : "fft_c64_") + std::to_string(N);
+    if (prof) {
+      if (a.mid) lab += "_spec";
+      if (a.tw_on) lab += a.tw_pre ? "_twin" : "_tw";
+      const bool pad = (a.g_mod - 1) + (N - 1) * a.gin_stride >= a.n_valid_in;
+      const bool trunc = (a.g_mod - 1) + (N - 1) * a.gout_stride >= a.n_valid_out;
+      if (a.pre || a.post || pad || trunc) lab += "_msk";
+    }
+    note(lab);
     if (!measure) launch_fft_tile(cdt, N, a, stream);
   }
   void wht(int d, int N, const WhtArgs& a) {

@@ -82,7 +82,7 @@ struct FftDev {
 enum : uint32_t {
   F_XREAL = 1, F_YREAL = 2, F_CONJX = 4, F_CONJY = 8, F_INV = 16, F_MIDCONJ = 32, F_TWINV = 64,
   F_ACC = 128, F_PRECONJ = 256, F_POSTCONJ = 512, F_PAD = 1024, F_TRUNC = 2048, F_SCALE = 4096,
-  F_GOFF = 8192
+  F_GOFF = 8192, F_TWPRE = 16384
 };
 
 struct WhtDev {
@@ -190,6 +190,11 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
           if (p.pre) {
             const C w = __ldg(&((const C*)p.pre)[g]);
             v = (f & F_PRECONJ) ? cmulc(v, w) : cmul(v, w);
+          }
+          if (f & F_TWPRE) {
+            const C w = tw2<C>((const C*)p.tw_hi, (const C*)p.tw_lo, p.tw_mask, p.tw_lo_bits,
+                               uint32_t(goff) * uint32_t(i));
+            v = (f & F_TWINV) ? cmulc(v, w) : cmul(v, w);
           }
           if (!MID && (f & F_INV)) v = conj(v);
         }
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
   const T* x = (const T*)p.x + xb;
   T* y = (T*)p.y + yb;
   T a[E];
-  constexpr int R0 = st_radix(N, E, 0, false);
+  constexpr int R0 = st_radix_lin(N, E, 0);
 #pragma unroll
   for (int u = 0; u < E / R0; ++u) {
     const int bb = j + u * TPC;
@@ -332,8 +337,8 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
     }
   }
   wht_stages<T, N, E, CT, 0>(a, sm, j, cs);
-  constexpr int RL = st_radix(N, E, NST - 1, false);
-  constexpr int NSL = st_ns(N, E, NST - 1, false);
+  constexpr int RL = st_radix_lin(N, E, NST - 1);
+  constexpr int NSL = st_ns_lin(N, E, NST - 1);
   if (!act) return;
 #pragma unroll
   for (int u = 0; u < E / RL; ++u) {
@@ -418,6 +423,7 @@ inline FftDev make_fft_dev(const FftArgs& a, int N) {
   if (gmax_out >= a.n_valid_out) f |= F_TRUNC;
   if (a.scale != 1.0) f |= F_SCALE;
   if (goff) f |= F_GOFF;
+  if (a.tw_on && a.tw_pre) f |= F_TWPRE;
   d.flags = f;
   return d;
 }
@@ -449,8 +455,9 @@ inline void fft_tile_launch(const FftArgs& a, cudaStream_t s) {
   const FftDev d = make_fft_dev(a, N);
   constexpr int CT = tile_CT(N, sizeof(C));
   const bool fast = (a.nb % CT) == 0 && !a.x_real && !a.y_real && !a.pre && !a.post && !a.accumulate &&
-                    !(d.flags & (F_PAD | F_TRUNC));
-  const bool mid = a.mid != nullptr, tw = a.tw_on != 0;
+                    !(d.flags & (F_PAD | F_TRUNC | F_TWPRE));
+  // (an input-side twiddle runs in the generic variant's load loop)
+  const bool mid = a.mid != nullptr, tw = a.tw_on != 0 && !a.tw_pre;
   if (mid && tw) fft_tile_go2<C, N, true, true>(d, a.nb, fast, s);
   else if (mid) fft_tile_go2<C, N, true, false>(d, a.nb, fast, s);
   else if (tw) fft_tile_go2<C, N, false, true>(d, a.nb, fast, s);

@@ -13,8 +13,35 @@ void launch_fft_tile_c64_large(int N, const FftArgs& a, cudaStream_t s);
 void launch_fft_tile_c128_small(int N, const FftArgs& a, cudaStream_t s);
 void launch_fft_tile_c128_large(int N, const FftArgs& a, cudaStream_t s);
 
-bool launch_fft_tma_c64(int N, const FftArgs& a, cudaStream_t s);
-bool launch_fft_tma_c128(int N, const FftArgs& a, cudaStream_t s);
+#define SMAT_TMA_DECL(P, N) bool launch_fft_tma_##P##_##N(const FftArgs& a, cudaStream_t s);
+SMAT_TMA_DECL(c64, 256)
+SMAT_TMA_DECL(c64, 512)
+SMAT_TMA_DECL(c64, 1024)
+SMAT_TMA_DECL(c64, 2048)
+SMAT_TMA_DECL(c128, 256)
+SMAT_TMA_DECL(c128, 512)
+SMAT_TMA_DECL(c128, 1024)
+SMAT_TMA_DECL(c128, 2048)
+#undef SMAT_TMA_DECL
+
+static bool launch_fft_tma_c64(int N, const FftArgs& a, cudaStream_t s) {
+  switch (N) {
+    case 256: return launch_fft_tma_c64_256(a, s);
+    case 512: return launch_fft_tma_c64_512(a, s);
+    case 1024: return launch_fft_tma_c64_1024(a, s);
+    case 2048: return launch_fft_tma_c64_2048(a, s);
+    default: return false;
+  }
+}
+static bool launch_fft_tma_c128(int N, const FftArgs& a, cudaStream_t s) {
+  switch (N) {
+    case 256: return launch_fft_tma_c128_256(a, s);
+    case 512: return launch_fft_tma_c128_512(a, s);
+    case 1024: return launch_fft_tma_c128_1024(a, s);
+    case 2048: return launch_fft_tma_c128_2048(a, s);
+    default: return false;
+  }
+}
 
 static bool tma_enabled() {
   static int on = -1;
@@ -26,7 +53,7 @@ static bool tma_enabled() {
 }
 
 void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
-  // persistent TMA-fed variant first (large tiles, unmasked complex passes)
+  // persistent TMA-fed variant first (large tiles, complex in and out)
   if (N >= 256 && tma_enabled()) {
     if (cdt == SMAT_C64 && launch_fft_tma_c64(N, a, s)) return;
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;

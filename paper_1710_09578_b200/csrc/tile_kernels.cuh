@@ -38,6 +38,8 @@ struct FftArgs {
   double scale = 1.0;
   int32_t x_real = 0, y_real = 0, conj_x = 0, conj_y = 0, inv = 0, mid_conj = 0;
   int32_t tw_on = 0, tw_inv = 0, accumulate = 0, pre_conj = 0, post_conj = 0;
+  // four-step twiddle on the input (W^(goff*i), after pre) instead of the output
+  int32_t tw_pre = 0;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).

@@ -27,7 +27,9 @@ namespace smat {
 template <class C, int N, int EP = 16, int NB = 0, bool TV = false, bool MS = false>
 struct TmaGeom {
   static constexpr int E = N < EP ? N : EP;
-  static constexpr int CT = tile_CT(N, sizeof(C));
+  // (double-precision 2048-point tiles: two columns, so that two landing
+  // buffers plus the spectrum slice or the four-step twiddles fit)
+  static constexpr int CT = sizeof(C) == 16 && N >= 2048 ? 2 : tile_CT(N, sizeof(C));
   static constexpr int TPC = N / E;
   static constexpr int T = TPC * CT;
   static constexpr int ROWB = CT * int(sizeof(C));                 // bytes per tile row
@@ -46,10 +48,17 @@ struct TmaGeom {
   static constexpr int MINB = (227 * 1024) / int(SMEM) >= 2 && 2 * T <= 1024 ? 2 : 1;
 };
 
-template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS>
+// MSK: the masked variant for the Bluestein / pruned-embedding passes — zero
+// padding of input rows (g = goff + i*gin_stride >= n_valid_in), truncation of
+// output rows, and the pre / post diagonal vectors indexed by g.  The tensor
+// maps cover rows i < ein (loads zero-fill the rest) and k < eout (stores drop
+// the rest); the few rows between ein and the tile's valid count are patched
+// with direct loads (stores) by the threads that own them.  goff is uniform
+// over a tile (launcher check), so the valid counts are per tile.
+template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK>
 __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, N, EP, NB, TW, MID>::MINB)
     fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
-                   const FftDev p, const int ntiles) {
+                   const FftDev p, const int ntiles, const int ein, const int eout) {
   using G = TmaGeom<C, N, EP, NB, TW, MID>;
   using R = typename RealOf<C>::T;
   constexpr int E = G::E, CT = G::CT, TPC = G::TPC, LAY = G::LAY;
@@ -69,9 +78,11 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
   const R sx = ((f & F_CONJX) != 0) != (!MID && (f & F_INV)) ? R(-1) : R(1);
   const bool pre_conj = MID || (f & F_INV);
   const bool twinv = (f & F_TWINV) != 0;
+  const bool twpre = TW && (f & F_TWPRE) != 0;  // twiddle the input instead of the output
   const R sc = (f & F_SCALE) ? R(p.scale) : R(1);
   const R s_re = sc;
-  const R s_im = ((f & F_CONJY) != 0) != (!TW && pre_conj) ? -sc : sc;
+  // (MSK: the inverse conjugation stays explicit, a post vector sits between it and conj_y)
+  const R s_im = ((f & F_CONJY) != 0) != (!TW && !MSK && pre_conj) ? -sc : sc;
   const R smid = (f & F_MIDCONJ) ? R(-1) : R(1);
 
   auto issue = [&](int t, int s) {
@@ -119,16 +130,24 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     }
   };
   if (int(blockIdx.x) < ntiles) tv_prefetch(blockIdx.x);
-  // shared copy of W_N from the global W_4096 table (stride 4096/N)
-  {
-    constexpr int st = 4096 / N;
+  // staged stage-twiddle table (st_twoff layout) from the global W_4096 table;
+  // the spectrum passes' mirrored inverse transform runs the same (palindromic)
+  // stage list and shares it
+  static_assert(!MID || st_palindrome(N, E), "spectrum pass needs a palindromic stage list");
+  for (int e = tid; e < N - R0; e += G::T) {
+    int t4096 = 0;
+#pragma unroll
+    for (int S = 1; S < NST; ++S) {
+      const int RS = st_radix(N, E, S, false), NS = st_ns(N, E, S, false), OFF = st_twoff(N, E, S, false);
+      if (e >= OFF && e < OFF + NS * (RS - 1)) {
+        const int k = (e - OFF) / (RS - 1), r = (e - OFF) % (RS - 1) + 1;
+        t4096 = (r * k * (4096 / (NS * RS))) & 4095;
+      }
+    }
     if constexpr (sizeof(C) == 8) {
-      const float4* g = reinterpret_cast<const float4*>(p.tw);
-      float4* s = reinterpret_cast<float4*>(tws);
-      for (int t = tid; t < N; t += G::T) s[t] = __ldg(&g[t * st]);
+      reinterpret_cast<float4*>(tws)[e] = __ldg(reinterpret_cast<const float4*>(p.tw) + t4096);
     } else {
-      const C* g = reinterpret_cast<const C*>(p.tw);
-      for (int t = tid; t < N; t += G::T) tws[t] = __ldg(&g[t * st]);
+      tws[e] = __ldg(reinterpret_cast<const C*>(p.tw) + t4096);
     }
   }
   __syncthreads();
@@ -143,6 +162,18 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     if (f & F_GOFF) {
       const uint32_t q = fdiv(b, p.gdiv.m, p.gdiv.s);
       goff = int32_t(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
+    }
+    // valid input rows i < vin, output rows k < vout of this tile
+    int vin = N, vout = N;
+    if constexpr (MSK) {
+      if (f & F_PAD) {
+        const int rem = p.n_valid_in - goff;
+        vin = rem <= 0 ? 0 : min(N, (rem + p.gin_stride - 1) / p.gin_stride);
+      }
+      if (f & F_TRUNC) {
+        const int rem = p.n_valid_out - goff;
+        vout = rem <= 0 ? 0 : min(N, (rem + p.gout_stride - 1) / p.gout_stride);
+      }
     }
     if constexpr (TW) {
       // goff is uniform over the tile's CT columns (launcher checks): the
@@ -161,6 +192,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
         }
       }
       if (t + gs < ntiles) tv_prefetch(t + gs);
+      if (twpre) __syncthreads();  // read right below, by other threads
     }
     // ---- stage 0 from the landing buffer (natural row order)
     const int sidx = it % G::NBUF;
@@ -171,7 +203,53 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     for (int u = 0; u < E / R0; ++u)
 #pragma unroll
       for (int r = 0; r < R0; ++r) a[u * R0 + r] = buf[(j + u * TPC + r * (N / R0)) * CT + cs];
-    if (sx < R(0)) {
+    if constexpr (MSK) {
+      // rows ein <= i < vin were zero-filled by the TMA box: load them directly
+      const C* xc = (const C*)p.x + (int64_t(o1) * p.xs1 + int64_t(o2) * p.xs2 + c);
+#pragma unroll
+      for (int u = 0; u < E / R0; ++u)
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+          const int i = j + u * TPC + r * (N / R0);
+          if (i >= ein && i < vin) a[u * R0 + r] = __ldg(&xc[int64_t(i) * p.xsi]);
+        }
+    }
+    if ((MSK && p.pre) || twpre) {
+      // conj_x, the pre vector, the input twiddle, then the inverse conjugation
+      if (f & F_CONJX) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
+      }
+      if constexpr (MSK) {
+        if (p.pre) {
+          const C* pv = (const C*)p.pre;
+          const bool pc = (f & F_PRECONJ) != 0;
+#pragma unroll
+          for (int u = 0; u < E / R0; ++u)
+#pragma unroll
+            for (int r = 0; r < R0; ++r) {
+              const int i = j + u * TPC + r * (N / R0);
+              if (i < vin) {
+                const C w = __ldg(&pv[goff + i * p.gin_stride]);
+                a[u * R0 + r] = pc ? cmulc(a[u * R0 + r], w) : cmul(a[u * R0 + r], w);
+              }
+            }
+        }
+      }
+      if constexpr (TW) {
+        if (twpre) {
+#pragma unroll
+          for (int u = 0; u < E / R0; ++u)
+#pragma unroll
+            for (int r = 0; r < R0; ++r)
+              a[u * R0 + r] = tw_mul<true>(a[u * R0 + r], tvs, j + u * TPC + r * (N / R0));
+        }
+      }
+      if (!MID && (f & F_INV)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
+      }
+    } else if (sx < R(0)) {
 #pragma unroll
       for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
     }
@@ -222,11 +300,29 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     for (int u = 0; u < E / RL; ++u) {
       const int bb = j + u * TPC;
       C* au = a + u * RL;
-      if constexpr (TW) {
+      if constexpr (TW || MSK) {
+        // (folded into s_im otherwise)
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
-          const C v = pre_conj ? conj(au[r]) : au[r];
-          au[r] = tw_mul<true>(v, tvs, bb + r * (N / RL));
+          C v = pre_conj ? conj(au[r]) : au[r];
+          if constexpr (TW) {
+            if (!twpre) v = tw_mul<true>(v, tvs, bb + r * (N / RL));
+          }
+          au[r] = v;
+        }
+      }
+      if constexpr (MSK) {
+        if (p.post) {
+          const C* qv = (const C*)p.post;
+          const bool qc = (f & F_POSTCONJ) != 0;
+#pragma unroll
+          for (int r = 0; r < RL; ++r) {
+            const int k = bb + r * (N / RL);
+            if (k < vout) {
+              const C w = __ldg(&qv[goff + k * p.gout_stride]);
+              au[r] = qc ? cmulc(au[r], w) : cmul(au[r], w);
+            }
+          }
         }
       }
       C* yk = yc + int64_t(bb) * p.ysi;
@@ -239,8 +335,14 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
       }
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        if constexpr (TS) buf[(bb + r * (N / RL)) * CT + cs] = au[r];
-        else yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+        const int k = bb + r * (N / RL);
+        if constexpr (TS) {
+          buf[k * CT + cs] = au[r];
+          // rows eout <= k < vout lie outside the store map: write them directly
+          if (MSK && k >= eout && k < vout) yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+        } else if (!MSK || k < vout) {
+          yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+        }
       }
     }
     if constexpr (!TS && TW) __syncthreads();  // tile twiddles are rebuilt next
@@ -278,51 +380,79 @@ inline bool tma_store_enabled() {
 template <class C, int N, int EP, int NB>
 inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   using G = TmaGeom<C, N, EP, NB>;
-  if (a.x_real || a.y_real || a.pre || a.post || a.accumulate) return false;
+  if (a.x_real || a.y_real || a.accumulate) return false;
   if (a.inner % G::CT != 0) return false;
-  // per-tile shared four-step twiddles / spectrum slices need goff uniform
-  // across a tile, and the slice must be contiguous
-  if ((a.tw_on || a.mid) && a.g_mod > 1 && (a.g_div % G::CT) != 0) return false;
-  if (a.mid && a.mid_stride != 1) return false;
   const FftDev d = make_fft_dev(a, N);
-  if (d.flags & (F_PAD | F_TRUNC)) return false;
+  const bool pad = (d.flags & F_PAD) != 0, trunc = (d.flags & F_TRUNC) != 0;
+  const bool msk = pad || trunc || a.pre || a.post;
+  // per-tile shared four-step twiddles / spectrum slices / valid row counts
+  // need goff uniform across a tile, and the slice must be contiguous
+  if ((a.tw_on || a.mid || msk) && a.g_mod > 1 && (a.g_div % G::CT) != 0) return false;
+  if (a.mid && a.mid_stride != 1) return false;
+  if (msk && (a.mid || a.gin_stride < 1 || a.gout_stride < 1)) return false;
+  // masked maps: rows split as (i % rlo, i / rlo) with the smallest rlo the
+  // 256-entry box limit allows, covering the rows valid for every tile
+  const int64_t rlo = N > 256 ? N / 256 : 1;
+  auto extent = [&](int64_t nv, int64_t gs) {
+    const int64_t rem = nv - (a.g_mod - 1);
+    int64_t v = rem <= 0 ? 0 : (rem + gs - 1) / gs;
+    if (v > N) v = N;
+    return (v / rlo) * rlo;
+  };
+  const int64_t ein = pad ? extent(a.n_valid_in, a.gin_stride) : N;
+  const int64_t eout = trunc ? extent(a.n_valid_out, a.gout_stride) : N;
+  if (ein == 0) return false;
   const int64_t n1 = a.nb / (a.n2 * a.inner);
   CUtensorMap map, ymap;
-  if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT)) return false;
+  if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT, pad ? rlo : 0,
+                     pad ? ein : 0))
+    return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
-  const bool ts = tma_store_enabled() &&
-                  make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT);
+  const bool ts = tma_store_enabled() && eout > 0 &&
+                  make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
+                                trunc ? rlo : 0, trunc ? eout : 0);
   if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag) {
-    constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value;
+  auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag, auto msk_tag) {
+    constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value,
+                   KV = decltype(msk_tag)::value;
     using GV = TmaGeom<C, N, EP, NB, TV, MV>;
-    const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
-    const int grid = int(ntiles < slots ? ntiles : slots);
-    auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV>;
-    set_smem(kern, GV::SMEM);
-    kern<<<grid, GV::T, GV::SMEM, s>>>(map, ymap, d, int(ntiles));
+    if constexpr (GV::SMEM > 232448) {
+      return false;  // does not fit one SM: per-tile kernel
+    } else {
+      const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
+      const int grid = int(ntiles < slots ? ntiles : slots);
+      auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV>;
+      set_smem(kern, GV::SMEM);
+      kern<<<grid, GV::T, GV::SMEM, s>>>(map, ymap, d, int(ntiles), int(ein), int(eout));
+      return true;
+    }
   };
-  auto pick2 = [&](auto ts_tag) {
-    if (a.mid && a.tw_on) pick(ts_tag, std::true_type{}, std::true_type{});
-    else if (a.mid) pick(ts_tag, std::true_type{}, std::false_type{});
-    else if (a.tw_on) pick(ts_tag, std::false_type{}, std::true_type{});
-    else pick(ts_tag, std::false_type{}, std::false_type{});
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  auto pick2 = [&](auto ts_tag) -> bool {
+    if (msk) {
+      if (a.tw_on) return pick(ts_tag, F_{}, T_{}, T_{});
+      return pick(ts_tag, F_{}, F_{}, T_{});
+    }
+    if (a.mid && a.tw_on) return pick(ts_tag, T_{}, T_{}, F_{});
+    if (a.mid) return pick(ts_tag, T_{}, F_{}, F_{});
+    if (a.tw_on) return pick(ts_tag, F_{}, T_{}, F_{});
+    return pick(ts_tag, F_{}, F_{}, F_{});
   };
-  if (ts) pick2(std::true_type{});
-  else pick2(std::false_type{});
-  SMAT_CUDA(cudaGetLastError());
-  return true;
+  const bool ok = ts ? pick2(T_{}) : pick2(F_{});
+  if (ok) SMAT_CUDA(cudaGetLastError());
+  return ok;
 }
 
 inline int tma_variant() {
   static int v = -1;
   if (v < 0) {
     // 1 (default): radix-32 stages, 3-deep landing ring, one CTA per SM
-    // 2: radix-32, single buffer, two CTAs per SM;  3: radix-16 stages
+    // 3: radix-16 stages
     const char* e = getenv("SMAT_TMA_VARIANT");
     v = e ? atoi(e) : 1;
   }
@@ -332,9 +462,10 @@ inline int tma_variant() {
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
   if constexpr (N >= 1024 && sizeof(C) == 8) {
-    const int v = tma_variant();
-    if (v == 1 || v == 0) return fft_tma_launch_v<C, N, 32, 3>(a, s);
-    if (v == 2) return fft_tma_launch_v<C, N, 32, 1>(a, s);
+    if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
+  }
+  if constexpr (N == 1024 && sizeof(C) == 16) {
+    if (tma_variant() == 2) return fft_tma_launch_v<C, N, 16, 1>(a, s);  // 2 CTAs/SM, one buffer each
   }
   return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }

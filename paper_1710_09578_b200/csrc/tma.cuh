@@ -100,14 +100,21 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // Tensor map of a block view  element (o1, o2, i, c) at p + o1*s1 + o2*s2 + i*si + c
 // (element size esz, a multiple of 8 bytes), i < N split as (i % 256, i / 256),
 // box = CT columns x all N rows of one (o1, o2).
+// Masked views (zero padding / truncation of the rows): rows = R < N makes the
+// map cover only rows i < R (R a multiple of rlo, i split as (i % rlo, i / rlo)):
+// loads zero-fill the rows beyond, stores drop them.
 inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n1, int64_t s1, int64_t n2,
-                          int64_t s2, int64_t N, int64_t si, int64_t inner, int CT) {
+                          int64_t s2, int64_t N, int64_t si, int64_t inner, int CT, int64_t rlo = 0,
+                          int64_t rows = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int64_t w = int64_t(esz / 8);  // 8-byte words per element
-  const int64_t rlo = N < 256 ? N : 256, rhi = N / rlo;
+  if (rlo == 0) rlo = N < 256 ? N : 256;
+  if (rows == 0) rows = N;
+  if (rlo > 256 || N / rlo > 256 || rows % rlo != 0 || rows <= 0) return false;
+  const int64_t rhi = rows / rlo;
   cuuint64_t dims[5] = {cuuint64_t(inner * w), cuuint64_t(rlo), cuuint64_t(rhi), cuuint64_t(n2), cuuint64_t(n1)};
-  cuuint64_t strides[4] = {cuuint64_t(si * int64_t(esz)), cuuint64_t(256 * si * int64_t(esz)),
+  cuuint64_t strides[4] = {cuuint64_t(si * int64_t(esz)), cuuint64_t(rlo * si * int64_t(esz)),
                            cuuint64_t(s2 * int64_t(esz)), cuuint64_t(s1 * int64_t(esz))};
   for (int k = 0; k < 4; ++k)
     if (strides[k] % 16 || strides[k] >= (cuuint64_t(1) << 40)) {
@@ -115,7 +122,7 @@ inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n
       strides[k] = 16;  // unused dimension of extent 1
     }
   if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return false;
-  cuuint32_t box[5] = {cuuint32_t(CT * w), cuuint32_t(rlo), cuuint32_t(rhi), 1, 1};
+  cuuint32_t box[5] = {cuuint32_t(CT * w), cuuint32_t(rlo), cuuint32_t(N / rlo), 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<void*>(p), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
