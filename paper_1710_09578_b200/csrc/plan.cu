@@ -112,6 +112,18 @@ __global__ void fourstep_perm_kernel(const double2* a, double2* b, int64_t N1, i
   }
 }
 
+// A length-n pre/post vector of a four-step transform of length Nt = N1*N2 in
+// per-tile order: out[n1*N2 + i] = v[n1 + N1*i] (0 past n), so the strided
+// passes (goff = n1, element i) read one contiguous slice per tile.
+template <class C>
+__global__ void fourstep_vec_kernel(const C* v, C* out, int64_t n, int64_t N1, int64_t N2) {
+  const int64_t tot = N1 * N2;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n1 = q / N2, i = q % N2, g = n1 + N1 * i;
+    out[q] = g < n ? v[g] : C{};
+  }
+}
+
 // S -> (S[2k], S[2k+1]) and the twiddles W_L^i (i < L/2) of the pruned
 // Toeplitz embedding.
 __global__ void split_even_odd_kernel(const double2* s, double2* se, double2* so, double2* tw, int64_t L) {
@@ -135,6 +147,21 @@ __global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
     const float c = float(a[i].x), s = float(a[i].y);
     b[i] = make_float4(c, s, -s, c);
   }
+}
+
+// Per-tile (four-step) copy of a pre/post vector of length n for transforms of
+// length Nt > kTileMax; nullptr when the transform is a single tile.
+static DevBuf* fourstep_vector(Plan& p, const DevBuf* v, int64_t n, int64_t Nt, int cdt) {
+  if (!v || Nt <= kTileMax) return nullptr;
+  int64_t N1, N2;
+  fourstep_split(Nt, N1, N2);
+  DevBuf* o = new_buf(p, cdt, Nt);
+  if (cdt == SMAT_C128)
+    fourstep_vec_kernel<double2><<<1184, 256>>>((const double2*)v->p, (double2*)o->p, n, N1, N2);
+  else
+    fourstep_vec_kernel<float2><<<1184, 256>>>((const float2*)v->p, (float2*)o->p, n, N1, N2);
+  SMAT_CUDA(cudaGetLastError());
+  return o;
 }
 
 // A convolution spectrum as the plan stores it: four-step order when it is
@@ -247,6 +274,10 @@ struct XformIO {
   bool mid_conj = false;
   const void* post = nullptr;
   bool post_conj = false;
+  // optional per-tile copies (fourstep_vector) of pre / post for the strided
+  // passes of a four-step convolution
+  const void* pre_fs = nullptr;
+  const void* post_fs = nullptr;
   bool conj_x = false, conj_y = false, inv = false, acc = false;
   double scale = 1.0;
 };
@@ -322,7 +353,12 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.g_div = ic; a.g_mod = N1; a.gin_stride = N1;
     a.n_valid_in = io.x_rows;
     a.pre = io.pre; a.pre_conj = io.pre_conj; a.conj_x = conj_first;
+    if (io.pre_fs) {
+      a.pre = io.pre_fs;
+      a.pre_gmul = N2;
+    }
     a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+    if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, false, true);
     c.fft(cdt, int(N2), a);
   }
   if (!io.mid) {
@@ -358,6 +394,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = 1; a.mid_gmul = N1;
       if (!tw3) {
         a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+        if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N1, true, true);
       }
       c.fft(cdt, int(N1), a);
     }
@@ -377,8 +414,13 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
         // pass 2's inverse twiddle W^-(n1*k2), applied to this pass's input
         a.tw_on = 1; a.tw_pre = 1; a.tw_inv = 1;
         a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+        if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, true, true);
       }
       a.post = io.post; a.post_conj = io.post_conj; a.conj_y = io.conj_y;
+      if (io.post_fs) {
+        a.post = io.post_fs;
+        a.post_gmul = N2;
+      }
       a.scale = io.scale; a.accumulate = io.acc;
       c.fft(cdt, int(N2), a);
     }
@@ -582,6 +624,7 @@ struct HadamardNode : Node {
 struct FourierNode : Node {
   int64_t n = 0, M = 0;
   DevBuf* chirp = nullptr;   // plan complex precision, length n
+  DevBuf* chirp_fs = nullptr;  // its per-tile copy (M > one tile)
   DevBuf* kspec = nullptr;   // FFT_M of the Bluestein kernel, length M
   std::string describe() const override {
     return "Fourier(" + std::to_string(n) + (M ? ", Bluestein M=" + std::to_string(M) : "") + ")";
@@ -596,6 +639,7 @@ struct FourierNode : Node {
       return;
     }
     io.pre = chirp->p; io.mid = kspec->p; io.post = chirp->p;
+    if (chirp_fs) io.pre_fs = io.post_fs = chirp_fs->p;
     io.scale = 1.0 / double(M);
     io.conj_x = adj; io.conj_y = adj;  // F^H y = conj(F conj(y))
     run_xform(c, M, g, io);
@@ -611,6 +655,8 @@ struct DiagFourierNode : Node {
   FourierNode* F = nullptr;
   DevBuf* vr = nullptr;  // applied before the transform (forward): chirp*dr or dr
   DevBuf* vl = nullptr;  // applied after it: chirp*dl or dl (may be the bare chirp)
+  DevBuf* vr_fs = nullptr;  // per-tile copies (transform longer than one tile)
+  DevBuf* vl_fs = nullptr;
   std::string describe() const override { return "DiagFourierDiag(" + F->describe() + ")"; }
   bool accepts_real() const override { return true; }
   void apply(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g, bool acc) override {
@@ -618,6 +664,8 @@ struct DiagFourierNode : Node {
     io.x = x; io.x_rows = F->n; io.y = y; io.y_rows = F->n; io.acc = acc;
     io.pre = (adj ? vl : vr) ? (adj ? vl : vr)->p : nullptr;
     io.post = (adj ? vr : vl) ? (adj ? vr : vl)->p : nullptr;
+    io.pre_fs = (adj ? vl_fs : vr_fs) ? (adj ? vl_fs : vr_fs)->p : nullptr;
+    io.post_fs = (adj ? vr_fs : vl_fs) ? (adj ? vr_fs : vl_fs)->p : nullptr;
     io.conj_x = adj; io.conj_y = adj;
     if (F->M) {
       io.mid = F->kspec->p;
@@ -1097,6 +1145,9 @@ struct Builder {
       DevBuf* chirp = F->M ? F->chirp : nullptr;
       n->vr = vec_product(chirp, dr ? dr->d : nullptr, cdt);
       n->vl = vec_product(chirp, dl ? dl->d : nullptr, cdt);
+      const int64_t Nt = F->M ? F->M : F->n;
+      n->vr_fs = fourstep_vector(p, n->vr, F->n, Nt, cdt);
+      n->vl_fs = fourstep_vector(p, n->vl, F->n, Nt, cdt);
       const size_t lo = dl ? i - 1 : i, hi = dr ? i + 1 : i;
       f.erase(f.begin() + lo, f.begin() + hi + 1);
       f.insert(f.begin() + lo, n);
@@ -1164,6 +1215,7 @@ struct Builder {
           device_fft_c128(p, n->M, ker->p, ks->p);
           n->chirp = narrow_c128(p, ch, cdt);
           n->kspec = spectrum_for_plan(p, ks, cdt);
+          n->chirp_fs = fourstep_vector(p, n->chirp, n->n, n->M, cdt);
         }
         out = n;
         break;

@@ -71,11 +71,13 @@ struct FftDev {
   const void* mid;
   int32_t mid_stride;
   int32_t mid_gmul;
+  int32_t pre_gmul, post_gmul;
   const void* tw;
   const void* tw_lo;
   const void* tw_hi;
   uint32_t tw_mask;
   int32_t tw_lo_bits;
+  const void* tw_slices;
   double scale;
   uint32_t flags;
 };
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
           v = (f & F_XREAL) ? mk(__ldg(&xr[off]), R(0)) : __ldg(&xc[off]);
           if (f & F_CONJX) v = conj(v);
           if (p.pre) {
-            const C w = __ldg(&((const C*)p.pre)[g]);
+            const C w = __ldg(&((const C*)p.pre)[p.pre_gmul ? goff * p.pre_gmul + i : g]);
             v = (f & F_PRECONJ) ? cmulc(v, w) : cmul(v, w);
           }
           if (f & F_TWPRE) {
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
         if (!TW && pre_conj) v = conj(v);
         if (act && (!(f & F_TRUNC) || g < p.n_valid_out)) {
           if (p.post) {
-            const C w = __ldg(&((const C*)p.post)[g]);
+            const C w = __ldg(&((const C*)p.post)[p.post_gmul ? goff * p.post_gmul + k : g]);
             v = (f & F_POSTCONJ) ? cmulc(v, w) : cmul(v, w);
           }
           if (f & F_CONJY) v = conj(v);
@@ -402,11 +404,16 @@ inline FftDev make_fft_dev(const FftArgs& a, int N) {
   d.mid = a.mid;
   d.mid_stride = int32_t(a.mid_stride);
   d.mid_gmul = int32_t(a.mid_gmul);
+  SMAT_CHECK(fits31((a.g_mod - 1) * a.pre_gmul + N) && fits31((a.g_mod - 1) * a.post_gmul + N), SMAT_UNSUPPORTED,
+             "fft tile: pre/post slice index exceeds 2^31");
+  d.pre_gmul = int32_t(a.pre_gmul);
+  d.post_gmul = int32_t(a.post_gmul);
   d.tw = a.tw;
   d.tw_lo = a.tw_lo;
   d.tw_hi = a.tw_hi;
   d.tw_mask = uint32_t(a.tw_mask);
   d.tw_lo_bits = a.tw_lo_bits;
+  d.tw_slices = a.tw_slices;
   d.scale = a.scale;
   uint32_t f = 0;
   if (a.x_real) f |= F_XREAL;

@@ -109,6 +109,38 @@ TwEntry tw_table(int device, int64_t n, int64_t count, int64_t step) {
 }
 }  // namespace
 
+// Per-tile four-step twiddle slices: entry g*E + e = W_nt^(g*e) (conjugated
+// for inv), one contiguous E-entry slice per tile offset g < nt/E; double2 or
+// the quad layout.  The angle is reduced exactly in integers.
+__global__ void tw_slice_kernel(double2* d, float4* q, int64_t nt, int64_t E, int inv) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nt; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = ((t / E) * (t % E)) % nt;
+    double s, c;
+    sincospi((inv ? 2.0 : -2.0) * double(m) / double(nt), &s, &c);
+    if (d) d[t] = make_double2(c, s);
+    if (q) q[t] = make_float4(float(c), float(s), -float(s), float(c));
+  }
+}
+
+namespace {
+std::unordered_map<uint64_t, void*> g_tws;
+}
+
+const void* twiddle_slices(int device, int64_t nt, int64_t E, bool inv, bool dbl) {
+  const uint64_t key = (uint64_t(device) << 58) ^ (uint64_t(ilog2(nt)) << 40) ^ (uint64_t(ilog2(E)) << 20) ^
+                       (uint64_t(inv) << 1) ^ uint64_t(dbl);
+  std::lock_guard<std::mutex> g(g_tw_mu);
+  auto it = g_tws.find(key);
+  if (it != g_tws.end()) return it->second;
+  void* p = nullptr;
+  SMAT_CUDA(cudaMalloc(&p, size_t(nt) * 16));
+  tw_slice_kernel<<<1184, 256>>>(dbl ? (double2*)p : nullptr, dbl ? nullptr : (float4*)p, nt, E, inv ? 1 : 0);
+  SMAT_CUDA(cudaGetLastError());
+  SMAT_CUDA(cudaDeviceSynchronize());
+  g_tws[key] = p;
+  return p;
+}
+
 const void* twiddle4096(int device, bool dbl) {
   TwEntry e = tw_table(device, 4096, 4096, 1);
   return dbl ? (const void*)e.d : (const void*)e.q;  // single precision: quad layout

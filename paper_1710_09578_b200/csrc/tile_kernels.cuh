@@ -40,6 +40,15 @@ struct FftArgs {
   int32_t tw_on = 0, tw_inv = 0, accumulate = 0, pre_conj = 0, post_conj = 0;
   // four-step twiddle on the input (W^(goff*i), after pre) instead of the output
   int32_t tw_pre = 0;
+  // pre / post vectors stored per tile ("four-step order"): when nonzero the
+  // entry of input row i (output row k) is pre[goff*pre_gmul + i]
+  // (post[goff*post_gmul + k]) instead of pre[g_in] (post[g_out]), so a tile's
+  // entries are one contiguous slice
+  int64_t pre_gmul = 0, post_gmul = 0;
+  // optional per-tile four-step twiddle slices (twiddle_slices with E = N,
+  // already conjugated for tw_inv): the TMA pass bulk-loads the tile's slice
+  // instead of assembling it from tw_lo / tw_hi
+  const void* tw_slices = nullptr;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).
@@ -74,5 +83,8 @@ struct TwPair {
   int lo_bits;
 };
 TwPair twiddle_pair(int device, int64_t ntot, bool dbl);
+// Per-tile four-step twiddle slices W_nt^(+-g*e) at g*E + e (16 bytes per entry:
+// double2, or the float quad layout), cached per device.
+const void* twiddle_slices(int device, int64_t nt, int64_t E, bool inv, bool dbl);
 
 }  // namespace smat

@@ -24,21 +24,27 @@ namespace smat {
 // EP: elements per thread (16 -> radix-16 stages, 32 -> radix-32 stages: one
 // exchange fewer for N = 1024); NB: landing buffers per CTA (0 = as many as fit,
 // up to 3).
-template <class C, int N, int EP = 16, int NB = 0, bool TV = false, bool MS = false>
+// CTO: columns per tile override (0 = default).
+template <class C, int N, int EP = 16, int NB = 0, bool TV = false, bool MS = false, int CTO = 0>
 struct TmaGeom {
   static constexpr int E = N < EP ? N : EP;
   // (double-precision 2048-point tiles: two columns, so that two landing
   // buffers plus the spectrum slice or the four-step twiddles fit)
-  static constexpr int CT = sizeof(C) == 16 && N >= 2048 ? 2 : tile_CT(N, sizeof(C));
+  static constexpr int CT = CTO ? CTO : sizeof(C) == 16 && N >= 2048 ? 2 : tile_CT(N, sizeof(C));
   static constexpr int TPC = N / E;
   static constexpr int T = TPC * CT;
   static constexpr int ROWB = CT * int(sizeof(C));                 // bytes per tile row
   static constexpr int LAY = ROWB >= 128 ? 1 : 128 / ROWB;          // exchange row permutation
   static constexpr size_t BUF = size_t(N) * CT * sizeof(C);         // one dense TMA box
   static constexpr size_t SPB = MS ? size_t(N) * 16 : 0;           // the tile's spectrum slice
-  static constexpr size_t STAGE = BUF + SPB;
+  // four-step twiddles: double precision bulk-loads the tile's slice of a
+  // precomputed table with the tile (TVSL); single precision assembles them
+  // per CTA from the two-level table (TVB)
+  static constexpr bool TVSL = TV && sizeof(C) == 16;
+  static constexpr size_t TVSB = TVSL ? size_t(N) * 16 : 0;
+  static constexpr size_t STAGE = BUF + SPB + TVSB;
   static constexpr size_t TWB = size_t(N) * 16;                    // W_N (float4 quads / double2)
-  static constexpr size_t TVB = TV ? size_t(N) * 16 : 0;           // per-tile four-step twiddles
+  static constexpr size_t TVB = TV && !TVSL ? size_t(N) * 16 : 0;  // per-tile four-step twiddles
   // ring of landing buffers: tile t computes in one while t+1.. load into the others
   static constexpr int NBUF =
       NB > 0 && (227 * 1024 - int(TWB + TVB) - 64) / int(STAGE) >= NB
@@ -48,18 +54,26 @@ struct TmaGeom {
   static constexpr int MINB = (227 * 1024) / int(SMEM) >= 2 && 2 * T <= 1024 ? 2 : 1;
 };
 
+// launcher-only flags of the TMA pass: the pre (post) vector is stored per
+// tile (pre_gmul / post_gmul) and rides with the tile as a bulk-loaded slice
+enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21 };
+
 // MSK: the masked variant for the Bluestein / pruned-embedding passes — zero
 // padding of input rows (g = goff + i*gin_stride >= n_valid_in), truncation of
-// output rows, and the pre / post diagonal vectors indexed by g.  The tensor
-// maps cover rows i < ein (loads zero-fill the rest) and k < eout (stores drop
-// the rest); the few rows between ein and the tile's valid count are patched
-// with direct loads (stores) by the threads that own them.  goff is uniform
-// over a tile (launcher check), so the valid counts are per tile.
-template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK>
-__global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, N, EP, NB, TW, MID>::MINB)
+// output rows, and the pre / post diagonal vectors.  The tensor maps cover rows
+// i < ein (loads zero-fill the rest) and k < eout (stores drop the rest); the
+// npatch rows from ein on that only some tiles own are loaded one tile ahead by
+// npatch*CT threads and written into the landing buffer, and output rows past
+// eout are stored directly by the threads that hold them.  A four-step-ordered
+// pre or post vector arrives as a slice in the stage's side area (like the
+// spectrum of the MID pass).  goff is uniform over a tile (launcher check), so
+// the valid counts are per tile.
+template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK, int CTO>
+__global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
+                                  TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::MINB)
     fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
-                   const FftDev p, const int ntiles, const int ein, const int eout) {
-  using G = TmaGeom<C, N, EP, NB, TW, MID>;
+                   const FftDev p, const int ntiles, const int ein, const int eout, const int npatch) {
+  using G = TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>;
   using R = typename RealOf<C>::T;
   constexpr int E = G::E, CT = G::CT, TPC = G::TPC, LAY = G::LAY;
   constexpr int NST = st_count(N, E);
@@ -70,6 +84,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
   // stage s: [tile data | spectrum slice] at smem_raw + s*STAGE
   auto stage_buf = [&](int s) { return reinterpret_cast<C*>(smem_raw + s * G::STAGE); };
   auto stage_spec = [&](int s) { return smem_raw + s * G::STAGE + G::BUF; };
+  auto stage_tv = [&](int s) { return reinterpret_cast<C*>(smem_raw + s * G::STAGE + G::BUF + G::SPB); };
+  constexpr bool TVSL = G::TVSL;
   C* tws = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE);  // W_N^t, t < N (float4 quads or double2)
   C* tvs = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE + G::TWB);  // four-step twiddles of the tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::NBUF * G::STAGE + G::TWB + G::TVB);
@@ -85,19 +101,50 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
   const R s_im = ((f & F_CONJY) != 0) != (!TW && !MSK && pre_conj) ? -sc : sc;
   const R smid = (f & F_MIDCONJ) ? R(-1) : R(1);
 
+  const bool side_pre = MSK && (f & F_SIDEPRE) != 0, side_post = MSK && (f & F_SIDEPOST) != 0;
+  auto tile_goff = [&](int t) -> int {
+    const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
+    return int(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
+  };
   auto issue = [&](int t, int s) {
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
-    mbar_arrive_expect_tx(&bars[s], uint32_t(G::BUF + G::SPB));
+    const uint32_t sb = MID ? uint32_t(N) * 16 : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
+    mbar_arrive_expect_tx(&bars[s], uint32_t(G::BUF + G::TVSB) + sb);
     tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
-    if constexpr (MID) {
-      // the tile's contiguous spectrum slice rides on the same barrier
-      const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
-      const uint32_t g = q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d;
-      bulk_load(stage_spec(s), reinterpret_cast<const unsigned char*>(p.mid) + size_t(g) * p.mid_gmul * 16,
-                uint32_t(G::SPB), &bars[s]);
+    if (sb || TVSL) {
+      // the tile's contiguous spectrum (or pre / post) and twiddle slices ride
+      // on the same barrier
+      const size_t g = size_t(tile_goff(t));
+      if (sb) {
+        const unsigned char* src =
+            MID ? reinterpret_cast<const unsigned char*>(p.mid) + g * p.mid_gmul * 16
+                : side_pre ? reinterpret_cast<const unsigned char*>(p.pre) + g * p.pre_gmul * sizeof(C)
+                           : reinterpret_cast<const unsigned char*>(p.post) + g * p.post_gmul * sizeof(C);
+        bulk_load(stage_spec(s), src, sb, &bars[s]);
+      }
+      if constexpr (TVSL)
+        bulk_load(stage_tv(s), reinterpret_cast<const unsigned char*>(p.tw_slices) + g * N * 16, uint32_t(G::TVSB),
+                  &bars[s]);
     }
   };
+  // rows ein .. ein+npatch-1: thread tid < npatch*CT owns row ein + tid/CT,
+  // column tid%CT, and loads it one tile ahead
+  const bool powner = MSK && tid < npatch * CT;
+  const int prow = ein + tid / CT, pcol = tid % CT;
+  auto patch_load = [&](int t) -> C {
+    uint32_t o1, o2, c0;
+    decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
+    int v = N;
+    if (f & F_PAD) {
+      const int rem = p.n_valid_in - tile_goff(t);
+      v = rem <= 0 ? 0 : min(N, (rem + p.gin_stride - 1) / p.gin_stride);
+    }
+    const C* xc = (const C*)p.x + (int64_t(o1) * p.xs1 + int64_t(o2) * p.xs2 + c0 + pcol);
+    return prow < v ? __ldg(&xc[int64_t(prow) * p.xsi]) : C{};
+  };
+  C pval{};
+  if (powner && int(blockIdx.x) < ntiles) pval = patch_load(blockIdx.x);
 
   // tiles are dealt round-robin (tile t = blockIdx.x + i*gridDim.x): at any
   // moment the CTAs work on neighbouring column groups of the same rows, so
@@ -113,9 +160,9 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
   // four-step twiddle software pipeline: the two-level table lookups of the
   // NEXT tile are issued during the current one
   constexpr int PER = (N + G::T - 1) / G::T;
-  C tvlo[TW ? PER : 1], tvhi[TW ? PER : 1];
+  C tvlo[TW && !TVSL ? PER : 1], tvhi[TW && !TVSL ? PER : 1];
   auto tv_prefetch = [&](int t) {
-    if constexpr (TW) {
+    if constexpr (TW && !TVSL) {
       const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
       const uint32_t g32 = q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d;
       const C* thi = (const C*)p.tw_hi;
@@ -175,7 +222,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
         vout = rem <= 0 ? 0 : min(N, (rem + p.gout_stride - 1) / p.gout_stride);
       }
     }
-    if constexpr (TW) {
+    if constexpr (TW && !TVSL) {
       // goff is uniform over the tile's CT columns (launcher checks): the
       // twiddles W^(goff*k) (conjugated for the inverse) are shared by all
       // columns — finish the lookups prefetched during the previous tile into
@@ -197,23 +244,22 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     // ---- stage 0 from the landing buffer (natural row order)
     const int sidx = it % G::NBUF;
     C* buf = stage_buf(sidx);
+    const C* tvt = TVSL ? stage_tv(sidx) : tvs;  // this tile's four-step twiddles
     mbar_wait(&bars[sidx], uint32_t((it / G::NBUF) & 1));
+    if constexpr (MSK) {
+      if (npatch > 0) {
+        // rows ein.. were zero-filled by the TMA box: drop in the prefetched
+        // values, then prefetch the next tile's
+        if (powner) buf[prow * CT + pcol] = pval;
+        __syncthreads();
+        if (powner && t + gs < ntiles) pval = patch_load(t + gs);
+      }
+    }
     C a[E];
 #pragma unroll
     for (int u = 0; u < E / R0; ++u)
 #pragma unroll
       for (int r = 0; r < R0; ++r) a[u * R0 + r] = buf[(j + u * TPC + r * (N / R0)) * CT + cs];
-    if constexpr (MSK) {
-      // rows ein <= i < vin were zero-filled by the TMA box: load them directly
-      const C* xc = (const C*)p.x + (int64_t(o1) * p.xs1 + int64_t(o2) * p.xs2 + c);
-#pragma unroll
-      for (int u = 0; u < E / R0; ++u)
-#pragma unroll
-        for (int r = 0; r < R0; ++r) {
-          const int i = j + u * TPC + r * (N / R0);
-          if (i >= ein && i < vin) a[u * R0 + r] = __ldg(&xc[int64_t(i) * p.xsi]);
-        }
-    }
     if ((MSK && p.pre) || twpre) {
       // conj_x, the pre vector, the input twiddle, then the inverse conjugation
       if (f & F_CONJX) {
@@ -223,6 +269,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
       if constexpr (MSK) {
         if (p.pre) {
           const C* pv = (const C*)p.pre;
+          const C* ps = reinterpret_cast<const C*>(stage_spec(sidx));
           const bool pc = (f & F_PRECONJ) != 0;
 #pragma unroll
           for (int u = 0; u < E / R0; ++u)
@@ -230,7 +277,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
             for (int r = 0; r < R0; ++r) {
               const int i = j + u * TPC + r * (N / R0);
               if (i < vin) {
-                const C w = __ldg(&pv[goff + i * p.gin_stride]);
+                const C w = side_pre ? ps[i] : __ldg(&pv[p.pre_gmul ? goff * p.pre_gmul + i : goff + i * p.gin_stride]);
                 a[u * R0 + r] = pc ? cmulc(a[u * R0 + r], w) : cmul(a[u * R0 + r], w);
               }
             }
@@ -242,7 +289,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
           for (int u = 0; u < E / R0; ++u)
 #pragma unroll
             for (int r = 0; r < R0; ++r)
-              a[u * R0 + r] = tw_mul<true>(a[u * R0 + r], tvs, j + u * TPC + r * (N / R0));
+              a[u * R0 + r] = tw_mul<true>(a[u * R0 + r], tvt, j + u * TPC + r * (N / R0));
         }
       }
       if (!MID && (f & F_INV)) {
@@ -286,9 +333,12 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
     }
     // all exchange reads of the landing buffer are done after this barrier
     __syncthreads();
+    // (the epilogue still reads a post slice or output twiddle slice of the stage)
+    const bool late_refill = side_post || (TVSL && !twpre);
     if constexpr (!TS) {
-      // the landing buffer is free: start the load NBUF tiles ahead
-      if (tid == 0 && t + G::NBUF * gs < ntiles) {
+      // the landing buffer is free: start the load NBUF tiles ahead (after the
+      // epilogue when it still reads the stage's side area)
+      if (!late_refill && tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
         issue(t + G::NBUF * gs, sidx);
       }
@@ -306,7 +356,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
         for (int r = 0; r < RL; ++r) {
           C v = pre_conj ? conj(au[r]) : au[r];
           if constexpr (TW) {
-            if (!twpre) v = tw_mul<true>(v, tvs, bb + r * (N / RL));
+            if (!twpre) v = tw_mul<true>(v, tvt, bb + r * (N / RL));
           }
           au[r] = v;
         }
@@ -314,12 +364,14 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
       if constexpr (MSK) {
         if (p.post) {
           const C* qv = (const C*)p.post;
+          const C* qs = reinterpret_cast<const C*>(stage_spec(sidx));
           const bool qc = (f & F_POSTCONJ) != 0;
 #pragma unroll
           for (int r = 0; r < RL; ++r) {
             const int k = bb + r * (N / RL);
             if (k < vout) {
-              const C w = __ldg(&qv[goff + k * p.gout_stride]);
+              const C w = side_post ? qs[k]
+                                    : __ldg(&qv[p.post_gmul ? goff * p.post_gmul + k : goff + k * p.gout_stride]);
               au[r] = qc ? cmulc(au[r], w) : cmul(au[r], w);
             }
           }
@@ -345,7 +397,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
         }
       }
     }
-    if constexpr (!TS && TW) __syncthreads();  // tile twiddles are rebuilt next
+    if constexpr (!TS) {
+      if (TW || late_refill) __syncthreads();  // tile twiddles are rebuilt next / side area read
+      if (late_refill && tid == 0 && t + G::NBUF * gs < ntiles) {
+        fence_proxy_async();
+        issue(t + G::NBUF * gs, sidx);
+      }
+    }
     if constexpr (TS) {
       fence_proxy_async();  // this thread's tile writes -> visible to the TMA engine
       __syncthreads();
@@ -354,8 +412,11 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID>::T, TmaGeom<C, 
         decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, q1, q2, c0);
         tma_store_5d(&ymap, buf, int(c0 * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
         bulk_commit();
+        // refill the buffer once the store has read it (deferring the refill
+        // into the next tile removes this wait but shortens the load lead by
+        // a tile, which measured slower)
         if (t + G::NBUF * gs < ntiles) {
-          bulk_wait_read0();  // the store has read the buffer: refill it
+          bulk_wait_read0();
           issue(t + G::NBUF * gs, sidx);
         }
       }
@@ -377,13 +438,13 @@ inline bool tma_store_enabled() {
   return v == 1;
 }
 
-template <class C, int N, int EP, int NB>
+template <class C, int N, int EP, int NB, int CTO = 0>
 inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
-  using G = TmaGeom<C, N, EP, NB>;
+  using G = TmaGeom<C, N, EP, NB, false, false, CTO>;
   if (a.x_real || a.y_real || a.accumulate) return false;
   if (a.inner % G::CT != 0) return false;
-  const FftDev d = make_fft_dev(a, N);
-  const bool pad = (d.flags & F_PAD) != 0, trunc = (d.flags & F_TRUNC) != 0;
+  const FftDev d0 = make_fft_dev(a, N);
+  const bool pad = (d0.flags & F_PAD) != 0, trunc = (d0.flags & F_TRUNC) != 0;
   const bool msk = pad || trunc || a.pre || a.post;
   // per-tile shared four-step twiddles / spectrum slices / valid row counts
   // need goff uniform across a tile, and the slice must be contiguous
@@ -402,6 +463,17 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   const int64_t ein = pad ? extent(a.n_valid_in, a.gin_stride) : N;
   const int64_t eout = trunc ? extent(a.n_valid_out, a.gout_stride) : N;
   if (ein == 0) return false;
+  // rows from ein that only some tiles own (the tile with goff = 0 owns the most)
+  int64_t npatch = 0;
+  if (pad) {
+    int64_t v0 = (a.n_valid_in + a.gin_stride - 1) / a.gin_stride;
+    if (v0 > N) v0 = N;
+    npatch = v0 - ein;
+    if (npatch * G::CT > G::T) return false;
+  }
+  FftDev d = d0;
+  if (msk && a.pre && a.pre_gmul) d.flags |= F_SIDEPRE;
+  else if (msk && a.post && a.post_gmul) d.flags |= F_SIDEPOST;
   const int64_t n1 = a.nb / (a.n2 * a.inner);
   CUtensorMap map, ymap;
   if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT, pad ? rlo : 0,
@@ -419,15 +491,18 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag, auto msk_tag) {
     constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value,
                    KV = decltype(msk_tag)::value;
-    using GV = TmaGeom<C, N, EP, NB, TV, MV>;
+    using GV = TmaGeom<C, N, EP, NB, TV, MV || KV, CTO>;
     if constexpr (GV::SMEM > 232448) {
       return false;  // does not fit one SM: per-tile kernel
+    } else if constexpr (MV && !st_palindrome(N, GV::E)) {
+      return false;  // the spectrum pass shares one staged table between its two transforms
     } else {
+      if (GV::TVSL && !a.tw_slices) return false;  // needs the precomputed twiddle slices
       const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
       const int grid = int(ntiles < slots ? ntiles : slots);
-      auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV>;
+      auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV, CTO>;
       set_smem(kern, GV::SMEM);
-      kern<<<grid, GV::T, GV::SMEM, s>>>(map, ymap, d, int(ntiles), int(ein), int(eout));
+      kern<<<grid, GV::T, GV::SMEM, s>>>(map, ymap, d, int(ntiles), int(ein), int(eout), int(npatch));
       return true;
     }
   };
@@ -461,11 +536,22 @@ inline int tma_variant() {
 
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
+  const int v = tma_variant();
   if constexpr (N >= 1024 && sizeof(C) == 8) {
-    if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
+    // 6: one buffer, two CTAs per SM;  7: same with 4-column tiles
+    if (v == 6) return fft_tma_launch_v<C, N, 32, 1>(a, s);
+    if (v == 7) return fft_tma_launch_v<C, N, 32, 1, 4>(a, s);
+    if (v == 10 && a.mid) return fft_tma_launch_v<C, N, 16, 0>(a, s);  // radix-16 spectrum pass
+    if (v != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
   }
   if constexpr (N == 1024 && sizeof(C) == 16) {
-    if (tma_variant() == 2) return fft_tma_launch_v<C, N, 16, 1>(a, s);  // 2 CTAs/SM, one buffer each
+    if (v == 2) return fft_tma_launch_v<C, N, 16, 1>(a, s);  // 2 CTAs/SM, one buffer each
+    if (v == 8) return fft_tma_launch_v<C, N, 16, 1, 2>(a, s);  // 2 CTAs/SM of 2-column tiles
+    // radix-8 stages: 512 threads per tile, half the registers per thread
+    if (v == 5 && !a.mid) return fft_tma_launch_v<C, N, 8, 0>(a, s);
+  }
+  if constexpr (N == 2048 && sizeof(C) == 16) {
+    if (v == 9) return fft_tma_launch_v<C, N, 16, 1, 1>(a, s);  // 2 CTAs/SM of 1-column tiles
   }
   return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }

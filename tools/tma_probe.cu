@@ -1,0 +1,126 @@
+// tma_probe.cu — copy bandwidth of TMA boxes vs box row width, to size the
+// FFT tile passes' column tiles.  A (rows x 2 KB) array is copied tile by tile
+// (W-byte x 256-row boxes, TMA load -> smem -> TMA store), persistent CTAs,
+// NB-deep ring; compared with a plain 16-byte LDG/STG copy of the same bytes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ uint32_t su(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+template <int W, int NB>
+__global__ void __launch_bounds__(128) tma_copy(const __grid_constant__ CUtensorMap in,
+                                                const __grid_constant__ CUtensorMap out, int ntiles, int ncolt) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NB * W * 256);
+  const int gs = gridDim.x;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < NB; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  auto issue = [&](int t, int s) {
+    const int c = (t % ncolt) * (W / 8), r = (t / ncolt) * 256;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&bar[s])), "r"(W * 256));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su(sm + s * W * 256)),
+        "l"(&in), "r"(c), "r"(r), "r"(su(&bar[s]))
+        : "memory");
+  };
+  for (int s = 0; s < NB; ++s)
+    if (blockIdx.x + s * gs < ntiles) issue(blockIdx.x + s * gs, s);
+  for (int t = blockIdx.x, it = 0; t < ntiles; t += gs, ++it) {
+    const int s = it % NB;
+    const uint32_t par = (it / NB) & 1;
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+            su(&bar[s])),
+        "r"(par)
+        : "memory");
+    const int c = (t % ncolt) * (W / 8), r = (t / ncolt) * 256;
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&out),
+                 "r"(su(sm + s * W * 256)), "r"(c), "r"(r)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;");
+    if (t + NB * gs < ntiles) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue(t + NB * gs, s);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void ldg_copy(const int4* in, int4* out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc() {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+}
+
+template <int W, int NB>
+static void run(void* a, void* b, size_t rows, int blocks_per_sm) {
+  CUtensorMap mi, mo;
+  cuuint64_t dims[2] = {256, rows};  // 2 KB rows of uint64
+  cuuint64_t str[1] = {2048};
+  cuuint32_t box[2] = {W / 8, 256};
+  cuuint32_t es[2] = {1, 1};
+  auto f = enc();
+  f(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, a, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, b, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const int ncolt = 2048 / W;
+  const int ntiles = int(rows / 256) * ncolt;
+  const size_t smem = size_t(NB) * W * 256 + 64;
+  cudaFuncSetAttribute(tma_copy<W, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const int grid = 148 * blocks_per_sm;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  tma_copy<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt);
+  cudaEventRecord(e0);
+  for (int k = 0; k < 5; ++k) tma_copy<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("TMA box %4d B x 256 rows, ring %d, %d CTA/SM (smem %zu KB): %7.1f GB/s  (%s)\n", W, NB, blocks_per_sm,
+         smem / 1024, 2.0 * rows * 2048 * 5 / (ms / 1e3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  const size_t rows = size_t(1) << 20;  // 2 GB
+  void *a, *b;
+  cudaMalloc(&a, rows * 2048);
+  cudaMalloc(&b, rows * 2048);
+  cudaMemset(a, 1, rows * 2048);
+  run<32, 4>(a, b, rows, 4);
+  run<64, 4>(a, b, rows, 2);
+  run<64, 4>(a, b, rows, 4);
+  run<64, 8>(a, b, rows, 2);
+  run<128, 4>(a, b, rows, 2);
+  run<128, 2>(a, b, rows, 4);
+  run<256, 2>(a, b, rows, 2);
+  run<256, 3>(a, b, rows, 1);
+  run<512, 1>(a, b, rows, 1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const size_t n = rows * 2048 / 16;
+  ldg_copy<<<148 * 8, 512>>>((const int4*)a, (int4*)b, n);
+  cudaEventRecord(e0);
+  for (int k = 0; k < 5; ++k) ldg_copy<<<148 * 8, 512>>>((const int4*)a, (int4*)b, n);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("LDG/STG int4 copy: %7.1f GB/s\n", 2.0 * rows * 2048 * 5 / (ms / 1e3) / 1e9);
+  return 0;
+}
