@@ -96,6 +96,22 @@ static DevBuf* narrow_c128(Plan& p, DevBuf* src, int cdt) {
   return d;
 }
 
+// Whether a transform of length Nt runs as a four-step decomposition (else one
+// tile pass).  Beyond one tile always; single-precision convolutions of more
+// than SMAT_FOURSTEP_C64CONV points (default 2048) too: a one-tile 4096-point
+// convolution keeps only 4 columns per CTA and is load-latency bound, while
+// its 64 x 64 four-step runs three passes of 256-byte-row tiles (for C3 the
+// intermediate lives mostly in L2).
+static bool fourstep(int64_t Nt, bool conv, int cdt) {
+  static int64_t lim = -1;
+  if (lim < 0) {
+    const char* e = getenv("SMAT_FOURSTEP_C64CONV");
+    lim = e ? atoll(e) : 2048;
+  }
+  if (Nt > kTileMax) return true;
+  return conv && cdt == SMAT_C64 && Nt > lim;
+}
+
 // Split of a four-step transform of length Nt = N1 * N2 (N1 = contiguous /
 // middle-pass length).  Must match run_xform.
 static void fourstep_split(int64_t Nt, int64_t& N1, int64_t& N2) {
@@ -164,13 +180,13 @@ static DevBuf* fourstep_vector(Plan& p, const DevBuf* v, int64_t n, int64_t Nt, 
   return o;
 }
 
-// A convolution spectrum as the plan stores it: four-step order when it is
-// longer than one tile (so the middle pass reads it contiguously per tile),
-// then in the plan's complex precision — double2 for complex128 plans, the
-// (w.x, w.y, -w.y, w.x) quad layout of cmul_q for complex64 plans.
+// A convolution spectrum as the plan stores it: four-step order when the
+// convolution runs four-step (so the middle pass reads it contiguously per
+// tile), then in the plan's complex precision — double2 for complex128 plans,
+// the (w.x, w.y, -w.y, w.x) quad layout of cmul_q for complex64 plans.
 static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
   DevBuf* s = src;
-  if (src->len > kTileMax) {
+  if (fourstep(src->len, true, cdt)) {
     int64_t N1, N2;
     fourstep_split(src->len, N1, N2);
     s = new_buf(p, SMAT_C128, src->len);
@@ -299,7 +315,7 @@ static bool tw_in_pass3(bool dbl, int64_t N1) {
 static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   const int cdt = cplx_of(c.dt);
   const bool dbl = cdt == SMAT_C128;
-  if (Nt <= kTileMax) {
+  if (!fourstep(Nt, io.mid != nullptr, cdt)) {
     FftArgs a;
     fill_views(a, io.x, io.y, g);
     xform_pass_common(a, c);
@@ -1272,7 +1288,12 @@ struct Builder {
         DevBuf* sp = new_buf(p, SMAT_C128, t->L);
         device_fft_c128(p, t->L, eb->p, sp->p);
         t->spec = spectrum_for_plan(p, sp, cdt);
-        if (t->L > kTileMax && t->L / 2 <= kTileMax && std::max(n, m) <= t->L / 2) {
+        // pruned halves only when each half is a single tile pass: once the
+        // halves go four-step too, one four-step convolution of length L moves
+        // fewer bytes (x read and y written once) in half the launches
+        const char* pe = getenv("SMAT_TOEPLITZ_PRUNE");
+        const bool prune = pe ? pe[0] == '1' : !fourstep(t->L / 2, true, cdt);
+        if (prune && t->L > kTileMax && t->L / 2 <= kTileMax && std::max(n, m) <= t->L / 2) {
           const int64_t h = t->L / 2;
           DevBuf* se = new_buf(p, SMAT_C128, h);
           DevBuf* so = new_buf(p, SMAT_C128, h);

@@ -14,6 +14,8 @@ void launch_fft_tile_c128_small(int N, const FftArgs& a, cudaStream_t s);
 void launch_fft_tile_c128_large(int N, const FftArgs& a, cudaStream_t s);
 
 #define SMAT_TMA_DECL(P, N) bool launch_fft_tma_##P##_##N(const FftArgs& a, cudaStream_t s);
+SMAT_TMA_DECL(c64, 64)
+SMAT_TMA_DECL(c64, 128)
 SMAT_TMA_DECL(c64, 256)
 SMAT_TMA_DECL(c64, 512)
 SMAT_TMA_DECL(c64, 1024)
@@ -26,6 +28,8 @@ SMAT_TMA_DECL(c128, 2048)
 
 static bool launch_fft_tma_c64(int N, const FftArgs& a, cudaStream_t s) {
   switch (N) {
+    case 64: return launch_fft_tma_c64_64(a, s);
+    case 128: return launch_fft_tma_c64_128(a, s);
     case 256: return launch_fft_tma_c64_256(a, s);
     case 512: return launch_fft_tma_c64_512(a, s);
     case 1024: return launch_fft_tma_c64_1024(a, s);
@@ -54,7 +58,12 @@ static bool tma_enabled() {
 
 void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
   // persistent TMA-fed variant first (large tiles, complex in and out)
-  if (N >= 256 && tma_enabled()) {
+  // (below 256 points only the four-step passes with twiddles / spectra /
+  // masks: the plain short passes run at HBM speed on the per-tile kernel)
+  const bool pad = (a.g_mod - 1) + (N - 1) * a.gin_stride >= a.n_valid_in;
+  const bool trunc = (a.g_mod - 1) + (N - 1) * a.gout_stride >= a.n_valid_out;
+  const bool extras = a.mid || a.tw_on || a.pre || a.post || pad || trunc;
+  if ((N >= 256 || (N >= 64 && extras)) && tma_enabled()) {
     if (cdt == SMAT_C64 && launch_fft_tma_c64(N, a, s)) return;
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;
   }

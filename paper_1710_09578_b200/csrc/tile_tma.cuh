@@ -51,7 +51,9 @@ struct TmaGeom {
           ? NB
           : ((227 * 1024 - int(TWB + TVB) - 64) / int(STAGE) >= 3 ? 3 : 2);
   static constexpr size_t SMEM = NBUF * STAGE + TWB + TVB + 64;
-  static constexpr int MINB = (227 * 1024) / int(SMEM) >= 2 && 2 * T <= 1024 ? 2 : 1;
+  // resident CTAs per SM: as many as shared memory and 1024 threads allow, up to 4
+  static constexpr int MB_S = (227 * 1024) / int(SMEM), MB_T = 1024 / T;
+  static constexpr int MINB = (MB_S < MB_T ? MB_S : MB_T) >= 4 ? 4 : (MB_S < MB_T ? MB_S : MB_T) >= 2 ? 2 : 1;
 };
 
 // launcher-only flags of the TMA pass: the pre (post) vector is stored per
@@ -110,7 +112,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
     const uint32_t sb = MID ? uint32_t(N) * 16 : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
-    mbar_arrive_expect_tx(&bars[s], uint32_t(G::BUF + G::TVSB) + sb);
+    // (a masked box moves only the ein rows every tile owns)
+    mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
     tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
     if (sb || TVSL) {
       // the tile's contiguous spectrum (or pre / post) and twiddle slices ride
@@ -259,7 +262,11 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
 #pragma unroll
     for (int u = 0; u < E / R0; ++u)
 #pragma unroll
-      for (int r = 0; r < R0; ++r) a[u * R0 + r] = buf[(j + u * TPC + r * (N / R0)) * CT + cs];
+      for (int r = 0; r < R0; ++r) {
+        // (rows past the tile's valid count were not loaded: zero padding)
+        const int i = j + u * TPC + r * (N / R0);
+        a[u * R0 + r] = (!MSK || i < vin) ? buf[i * CT + cs] : C{};
+      }
     if ((MSK && p.pre) || twpre) {
       // conj_x, the pre vector, the input twiddle, then the inverse conjugation
       if (f & F_CONJX) {
@@ -477,12 +484,12 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   const int64_t n1 = a.nb / (a.n2 * a.inner);
   CUtensorMap map, ymap;
   if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT, pad ? rlo : 0,
-                     pad ? ein : 0))
+                     pad ? ein : 0, pad))
     return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
   const bool ts = tma_store_enabled() && eout > 0 &&
                   make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
-                                trunc ? rlo : 0, trunc ? eout : 0);
+                                trunc ? rlo : 0, trunc ? eout : 0, trunc);
   if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;
@@ -547,13 +554,17 @@ inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
   if constexpr (N == 1024 && sizeof(C) == 16) {
     if (v == 2) return fft_tma_launch_v<C, N, 16, 1>(a, s);  // 2 CTAs/SM, one buffer each
     if (v == 8) return fft_tma_launch_v<C, N, 16, 1, 2>(a, s);  // 2 CTAs/SM of 2-column tiles
+    if (v == 11) return fft_tma_launch_v<C, N, 32, 1>(a, s);  // radix-32, 128 threads, 2 CTAs/SM
     // radix-8 stages: 512 threads per tile, half the registers per thread
     if (v == 5 && !a.mid) return fft_tma_launch_v<C, N, 8, 0>(a, s);
   }
   if constexpr (N == 2048 && sizeof(C) == 16) {
     if (v == 9) return fft_tma_launch_v<C, N, 16, 1, 1>(a, s);  // 2 CTAs/SM of 1-column tiles
   }
-  return fft_tma_launch_v<C, N, 16, 0>(a, s);
+  // short transforms: radix-8 stages (palindromic lists for 64 and 128, so the
+  // spectrum pass qualifies), several CTAs per SM
+  if constexpr (N < 256) return fft_tma_launch_v<C, N, 8, 0>(a, s);
+  else return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }
 
 }  // namespace smat

@@ -1,0 +1,9 @@
+// tile_tma_c64_128.cu — 128-point instantiations of the persistent TMA-fed FFT
+// tile pass (float2); one file per length so they compile in parallel.
+#include "tile_tma.cuh"
+
+namespace smat {
+
+bool launch_fft_tma_c64_128(const FftArgs& a, cudaStream_t s) { return fft_tma_launch<float2, 128>(a, s); }
+
+}  // namespace smat

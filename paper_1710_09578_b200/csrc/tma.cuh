@@ -101,11 +101,13 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // (element size esz, a multiple of 8 bytes), i < N split as (i % 256, i / 256),
 // box = CT columns x all N rows of one (o1, o2).
 // Masked views (zero padding / truncation of the rows): rows = R < N makes the
-// map cover only rows i < R (R a multiple of rlo, i split as (i % rlo, i / rlo)):
-// loads zero-fill the rows beyond, stores drop them.
+// map cover only rows i < R (R a multiple of rlo, i split as (i % rlo, i / rlo));
+// with box_rows = R the box moves only those rows (the kernel treats the rest
+// of the tile as zero / does not store it), otherwise loads zero-fill the rows
+// beyond and stores drop them.
 inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n1, int64_t s1, int64_t n2,
                           int64_t s2, int64_t N, int64_t si, int64_t inner, int CT, int64_t rlo = 0,
-                          int64_t rows = 0) {
+                          int64_t rows = 0, bool box_rows = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int64_t w = int64_t(esz / 8);  // 8-byte words per element
@@ -122,7 +124,7 @@ inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n
       strides[k] = 16;  // unused dimension of extent 1
     }
   if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return false;
-  cuuint32_t box[5] = {cuuint32_t(CT * w), cuuint32_t(rlo), cuuint32_t(N / rlo), 1, 1};
+  cuuint32_t box[5] = {cuuint32_t(CT * w), cuuint32_t(rlo), cuuint32_t(box_rows ? rhi : N / rlo), 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<void*>(p), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

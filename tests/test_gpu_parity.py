@@ -190,6 +190,33 @@ def test_large_four_step_fft_and_bluestein():
         _close(op.forward(x.astype(np.complex64)), orc.dft(x), 1e-5, f"F{n} c64")
 
 
+def test_convolution_plan_shapes():
+    """The structurally different convolution plans against the oracle:
+    single precision Toeplitz with L = 8192 runs one four-step convolution of
+    64-point TMA passes (masked pad / truncate), double precision runs the two
+    pruned 4096-point halves; a 4096-point complex64 Circulant runs four-step;
+    rectangular Toeplitz (rows != cols) exercises the asymmetric masks."""
+    rng = np.random.default_rng(21)
+    for n, m, dt in ((3000, 3000, np.float32), (3000, 3000, np.float64), (2500, 3100, np.float32),
+                     (3100, 2100, np.float64), (1500, 4000, np.float32)):
+        col = rng.standard_normal(n)
+        row = rng.standard_normal(m - 1)
+        op = sm.Toeplitz(col.astype(dt), row.astype(dt))
+        ref = orc.toeplitz(col, row)
+        x = rng.standard_normal((m, 6))
+        y = rng.standard_normal((n, 6))
+        tol = TOL[dt]
+        _close(op.forward(x.astype(dt)), orc.apply(ref, x), tol, f"T{n}x{m} {dt.__name__} fwd")
+        _close(op.backward(y.astype(dt)), orc.apply(ref, y, 1), tol, f"T{n}x{m} {dt.__name__} bwd")
+    for n in (4096, 2048, 64, 128):
+        c = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        x = rng.standard_normal((n, 8)) + 1j * rng.standard_normal((n, 8))
+        op = sm.Circulant(c.astype(np.complex64))
+        ref = orc.circulant(c)
+        _close(op.forward(x.astype(np.complex64)), orc.apply(ref, x), 1e-5, f"C{n} c64 fwd")
+        _close(op.backward(x.astype(np.complex64)), orc.apply(ref, x, 1), 1e-5, f"C{n} c64 bwd")
+
+
 def test_adjoint_identity_random_ops():
     rng = np.random.default_rng(5)
     ops = [sm.Fourier(1000), sm.Circulant(rng.standard_normal(5000)),

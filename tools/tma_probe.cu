@@ -52,6 +52,100 @@ __global__ void __launch_bounds__(128) tma_copy(const __grid_constant__ CUtensor
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Strided variant: the array is M rows of 2 KB viewed as row = n1 + N1*i; a
+// tile is W bytes x 256 rows i of one n1 (the access pattern of the strided
+// four-step passes: row stride N1 * 2 KB).  Tiles are dealt column-tile first,
+// then n1, then the i block.
+template <int W, int NB>
+__global__ void __launch_bounds__(128) tma_copy3(const __grid_constant__ CUtensorMap in,
+                                                 const __grid_constant__ CUtensorMap out, int ntiles, int ncolt,
+                                                 int n1s, int order) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NB * W * 256);
+  const int gs = gridDim.x;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < NB; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  auto coords = [&](int t, int& c, int& n1, int& ib) {
+    if (order == 0) {  // column tile fastest, then n1, then the row block
+      c = (t % ncolt) * (W / 8);
+      n1 = (t / ncolt) % n1s;
+      ib = (t / ncolt / n1s) * 256;
+    } else {  // n1 fastest
+      n1 = t % n1s;
+      c = ((t / n1s) % ncolt) * (W / 8);
+      ib = (t / n1s / ncolt) * 256;
+    }
+  };
+  auto issue = [&](int t, int s) {
+    int c, n1, ib;
+    coords(t, c, n1, ib);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&bar[s])), "r"(W * 256));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(su(sm + s * W * 256)),
+        "l"(&in), "r"(c), "r"(n1), "r"(ib), "r"(su(&bar[s]))
+        : "memory");
+  };
+  for (int s = 0; s < NB; ++s)
+    if (blockIdx.x + s * gs < ntiles) issue(blockIdx.x + s * gs, s);
+  for (int t = blockIdx.x, it = 0; t < ntiles; t += gs, ++it) {
+    const int s = it % NB;
+    const uint32_t par = (it / NB) & 1;
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+            su(&bar[s])),
+        "r"(par)
+        : "memory");
+    int c, n1, ib;
+    coords(t, c, n1, ib);
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&out),
+                 "r"(su(sm + s * W * 256)), "r"(c), "r"(n1), "r"(ib)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;");
+    if (t + NB * gs < ntiles) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue(t + NB * gs, s);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc();
+
+template <int W, int NB>
+static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int order = 0) {
+  CUtensorMap mi, mo;
+  const size_t n2 = rows / n1s;
+  cuuint64_t dims[3] = {256, cuuint64_t(n1s), n2};
+  cuuint64_t str[2] = {2048, cuuint64_t(n1s) * 2048};
+  cuuint32_t box[3] = {W / 8, 1, 256};
+  cuuint32_t es[3] = {1, 1, 1};
+  auto f = enc();
+  f(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, a, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, b, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const int ncolt = 2048 / W;
+  const int ntiles = int(n2 / 256) * n1s * ncolt;
+  const size_t smem = size_t(NB) * W * 256 + 64;
+  cudaFuncSetAttribute(tma_copy3<W, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const int grid = 148 * blocks_per_sm;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order);
+  cudaEventRecord(e0);
+  for (int k = 0; k < 3; ++k) tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("strided TMA box %4d B x 256 rows, row stride %8zu KB, order %d, ring %d, %d CTA/SM: %7.1f GB/s  (%s)\n", W,
+         size_t(n1s) * 2, order, NB, blocks_per_sm, 2.0 * double(n2 / 256 * 256) * n1s * 2048 * 3 / (ms / 1e3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 __global__ void ldg_copy(const int4* in, int4* out, size_t n) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     out[i] = in[i];
@@ -110,6 +204,11 @@ int main() {
   run<256, 2>(a, b, rows, 2);
   run<256, 3>(a, b, rows, 1);
   run<512, 1>(a, b, rows, 1);
+  // strided rows (four-step passes): 64-byte rows at 2 KB .. 4 MB stride
+  for (int n1s : {1, 8, 256, 2048}) run3<64, 4>(a, b, rows, n1s, 2);
+  for (int n1s : {1, 256, 2048}) run3<128, 4>(a, b, rows, n1s, 2);
+  // padded strides: 4 MB + 2 KB * (n1s - 2048)
+  for (int n1s : {2049, 2064, 2080, 2112, 2304, 3072}) run3<64, 4>(a, b, rows - rows % n1s, n1s, 2);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
