@@ -18,9 +18,13 @@ def label(kernel: str):
     m = re.search(r"fft_(?:tma|tile)_kernel<(float2|double2), (\d+)", kernel)
     if m:
         return ("fft_c64_" if m.group(1) == "float2" else "fft_c128_") + m.group(2)
-    m = re.search(r"wht_tile_kernel<[^,]+, (\d+)>", kernel)
+    m = re.search(r"wht_tile_kernel<[^,]+, (\d+)", kernel)
     if m:
         return "wht_" + m.group(1)
+    if "lr_contract_kernel" in kernel:
+        return "lowrank_contract"
+    if "lr_expand_kernel" in kernel:
+        return "lowrank_expand"
     for k in ("gemm", "point", "gather", "scatter"):
         if f"{k}_kernel" in kernel:
             return k
