@@ -404,8 +404,11 @@ def run_native(args, cfg):
     if not args.no_e2e:
         Xh = X.cpu().pin_memory()
         e_steps = max(3, min(args.steps, 5))
-        yh = op.forward(Xh)
-        op.backward(yh)
+        # two untimed steps in the timed loop's exact pattern, so the pinned
+        # host caching allocator holds every output block the loop cycles through
+        for _ in range(2):
+            yh = op.forward(Xh)
+            zh = op.backward(yh)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
