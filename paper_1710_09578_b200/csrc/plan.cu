@@ -302,6 +302,15 @@ static void xform_pass_common(FftArgs& a, Ctx& c) {
   a.tw = twiddle4096(c.device, cplx_of(c.dt) == SMAT_C128);
 }
 
+static bool blocked_w() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SMAT_BLOCKED_W");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static bool tw_in_pass3(bool dbl, int64_t N1) {
   static int force = -2;
   if (force == -2) {
@@ -357,8 +366,35 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   gw.n2 = O;
   gw.inner = ic;
   Blk W = c.alloc_blk(cdt, gw, Nt);
+  // Blocked intermediate (single outer batch): logical row n1 + N1*k2 of W is
+  // stored at ((n1 / B)*N2 + k2)*B + n1 % B, B = 64 — the strided passes then
+  // walk W with a B-row stride and the middle pass reads B contiguous rows
+  // per block, instead of both walking N1*K-element strides that put every
+  // row in its own 2 MB page (translation-bound, tools/tma_probe.cu).  Only
+  // the user-layout side of the outer passes stays strided.
+  const bool blk = O == 1 && N1 >= 128 && blocked_w();
+  constexpr int BL = 6;
+  const int64_t B = int64_t(1) << BL;
   // ---- pass 1: x -> W
-  {
+  if (blk) {
+    FftArgs a;
+    xform_pass_common(a, c);
+    a.x = io.x.p; a.x_real = !dt_complex(io.x.dt);
+    a.xs1 = B * io.x.si; a.xs2 = io.x.si; a.xsi = N1 * io.x.si;  // (n1 / B, n1 % B, k2)
+    a.y = W.p; a.y_real = 0;
+    a.ys1 = N2 * B * ic; a.ys2 = ic; a.ysi = B * ic;
+    a.n2 = B; a.inner = ic; a.nb = N1 * ic;
+    a.g_div = ic; a.g_mod = N1; a.gin_stride = N1;
+    a.n_valid_in = io.x_rows;
+    a.pre = io.pre; a.pre_conj = io.pre_conj; a.conj_x = conj_first;
+    if (io.pre_fs) {
+      a.pre = io.pre_fs;
+      a.pre_gmul = N2;
+    }
+    a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
+    if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, false, true);
+    c.fft(cdt, int(N2), a);
+  } else {
     FftArgs a;
     xform_pass_common(a, c);
     a.x = io.x.p; a.x_real = !dt_complex(io.x.dt);
@@ -385,6 +421,10 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.xs1 = W.s2; a.xs2 = N1 * ic; a.xsi = ic;
     a.y = io.y.p; a.y_real = !dt_complex(io.y.dt);
     a.ys1 = io.y.s2; a.ys2 = io.y.si; a.ysi = N2 * io.y.si;
+    if (blk) {  // W rows n1 of block k2: B contiguous, then N2*B rows apart
+      a.xs2 = B * ic;
+      a.i_lo_bits = BL; a.xsi_hi = N2 * B * ic; a.ysi_hi = B * a.ysi;
+    }
     a.n2 = N2; a.inner = ic; a.nb = O * N2 * ic;
     a.g_div = ic; a.g_mod = N2; a.gout_stride = N2;
     a.n_valid_out = io.y_rows;
@@ -403,6 +443,10 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.x = W.p; a.y = W.p;
       a.xs1 = W.s2; a.xs2 = N1 * ic; a.xsi = ic;
       a.ys1 = W.s2; a.ys2 = N1 * ic; a.ysi = ic;
+      if (blk) {
+        a.xs2 = a.ys2 = B * ic;
+        a.i_lo_bits = BL; a.xsi_hi = a.ysi_hi = N2 * B * ic;
+      }
       a.n2 = N2; a.inner = ic; a.nb = O * N2 * ic;
       a.g_div = ic; a.g_mod = N2;
       // spectra longer than one tile are stored in four-step order
@@ -423,6 +467,11 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.y = io.y.p; a.y_real = !dt_complex(io.y.dt);
       a.ys1 = 0; a.ys2 = io.y.s2; a.ysi = N1 * io.y.si;
       a.n2 = O; a.inner = N1 * ic; a.nb = O * N1 * ic;
+      if (blk) {  // (n1 / B, n1 % B, k2) as in pass 1
+        a.xs1 = N2 * B * ic; a.xs2 = ic; a.xsi = B * ic;
+        a.ys1 = B * io.y.si; a.ys2 = io.y.si; a.ysi = N1 * io.y.si;
+        a.n2 = B; a.inner = ic; a.nb = N1 * ic;
+      }
       a.g_div = ic; a.g_mod = N1; a.gout_stride = N1;
       a.n_valid_out = io.y_rows;
       a.inv = 1;

@@ -78,9 +78,15 @@ struct FftDev {
   uint32_t tw_mask;
   int32_t tw_lo_bits;
   const void* tw_slices;
+  int64_t xsi_hi, ysi_hi;  // two-level row strides (i_lo_bits > 0)
+  int32_t i_lo_bits;
   double scale;
   uint32_t flags;
 };
+// Element offset of row i (two-level when lo_bits > 0).
+__device__ __forceinline__ int64_t row_off(int i, int32_t si, int64_t si_hi, int lo_bits) {
+  return lo_bits ? int64_t(i & ((1 << lo_bits) - 1)) * si + int64_t(i >> lo_bits) * si_hi : int64_t(i) * si;
+}
 enum : uint32_t {
   F_XREAL = 1, F_YREAL = 2, F_CONJX = 4, F_CONJY = 8, F_INV = 16, F_MIDCONJ = 32, F_TWINV = 64,
   F_ACC = 128, F_PRECONJ = 256, F_POSTCONJ = 512, F_PAD = 1024, F_TRUNC = 2048, F_SCALE = 4096,
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
         C v = mk(R(0), R(0));
         const int g = goff + i * p.gin_stride;
         if (act && (!(f & F_PAD) || g < p.n_valid_in)) {
-          const int64_t off = int64_t(i) * p.xsi;
+          const int64_t off = row_off(i, p.xsi, p.xsi_hi, p.i_lo_bits);
           v = (f & F_XREAL) ? mk(__ldg(&xr[off]), R(0)) : __ldg(&xc[off]);
           if (f & F_CONJX) v = conj(v);
           if (p.pre) {
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
           }
           if (f & F_CONJY) v = conj(v);
           if (f & F_SCALE) v = scl(v, sc);
-          const int64_t off = int64_t(k) * p.ysi;
+          const int64_t off = row_off(k, p.ysi, p.ysi_hi, p.i_lo_bits);
           if (f & F_YREAL) {
             yr[off] = (f & F_ACC) ? yr[off] + v.x : v.x;
           } else {
@@ -414,6 +420,9 @@ inline FftDev make_fft_dev(const FftArgs& a, int N) {
   d.tw_mask = uint32_t(a.tw_mask);
   d.tw_lo_bits = a.tw_lo_bits;
   d.tw_slices = a.tw_slices;
+  d.i_lo_bits = a.i_lo_bits;
+  d.xsi_hi = a.i_lo_bits ? a.xsi_hi : 0;
+  d.ysi_hi = a.i_lo_bits ? a.ysi_hi : 0;
   d.scale = a.scale;
   uint32_t f = 0;
   if (a.x_real) f |= F_XREAL;
@@ -462,7 +471,7 @@ inline void fft_tile_launch(const FftArgs& a, cudaStream_t s) {
   const FftDev d = make_fft_dev(a, N);
   constexpr int CT = tile_CT(N, sizeof(C));
   const bool fast = (a.nb % CT) == 0 && !a.x_real && !a.y_real && !a.pre && !a.post && !a.accumulate &&
-                    !(d.flags & (F_PAD | F_TRUNC | F_TWPRE));
+                    !(d.flags & (F_PAD | F_TRUNC | F_TWPRE)) && a.i_lo_bits == 0;
   // (an input-side twiddle runs in the generic variant's load loop)
   const bool mid = a.mid != nullptr, tw = a.tw_on != 0 && !a.tw_pre;
   if (mid && tw) fft_tile_go2<C, N, true, true>(d, a.nb, fast, s);

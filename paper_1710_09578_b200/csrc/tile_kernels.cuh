@@ -49,6 +49,10 @@ struct FftArgs {
   // already conjugated for tw_inv): the TMA pass bulk-loads the tile's slice
   // instead of assembling it from tw_lo / tw_hi
   const void* tw_slices = nullptr;
+  // two-level row strides (blocked four-step intermediates): when i_lo_bits
+  // > 0, row i of x sits at (i % 2^b)*xsi + (i >> b)*xsi_hi, likewise for y
+  int32_t i_lo_bits = 0;
+  int64_t xsi_hi = 0, ysi_hi = 0;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).

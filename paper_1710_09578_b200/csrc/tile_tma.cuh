@@ -482,14 +482,19 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   if (msk && a.pre && a.pre_gmul) d.flags |= F_SIDEPRE;
   else if (msk && a.post && a.post_gmul) d.flags |= F_SIDEPOST;
   const int64_t n1 = a.nb / (a.n2 * a.inner);
+  // two-level rows (blocked four-step intermediate): the row split of the map
+  // is the blocking itself; masks and direct row accesses stay single-level
+  const int64_t blo = a.i_lo_bits ? (int64_t(1) << a.i_lo_bits) : 0;
+  if (blo && (msk || blo > 256 || N / blo > 256 || N % blo)) return false;
   CUtensorMap map, ymap;
-  if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT, pad ? rlo : 0,
-                     pad ? ein : 0, pad))
+  if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT,
+                     blo ? blo : pad ? rlo : 0, pad ? ein : 0, pad, blo ? a.xsi_hi : 0))
     return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
   const bool ts = tma_store_enabled() && eout > 0 &&
                   make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
-                                trunc ? rlo : 0, trunc ? eout : 0, trunc);
+                                blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc, blo ? a.ysi_hi : 0);
+  if (!ts && blo) return false;  // direct stores are single-level
   if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;

@@ -105,9 +105,10 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // with box_rows = R the box moves only those rows (the kernel treats the rest
 // of the tile as zero / does not store it), otherwise loads zero-fill the rows
 // beyond and stores drop them.
+// Two-level rows (si_hi > 0): row i at (i % rlo)*si + (i / rlo)*si_hi.
 inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n1, int64_t s1, int64_t n2,
                           int64_t s2, int64_t N, int64_t si, int64_t inner, int CT, int64_t rlo = 0,
-                          int64_t rows = 0, bool box_rows = false) {
+                          int64_t rows = 0, bool box_rows = false, int64_t si_hi = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int64_t w = int64_t(esz / 8);  // 8-byte words per element
@@ -116,7 +117,8 @@ inline bool make_view_map(CUtensorMap* map, const void* p, size_t esz, int64_t n
   if (rlo > 256 || N / rlo > 256 || rows % rlo != 0 || rows <= 0) return false;
   const int64_t rhi = rows / rlo;
   cuuint64_t dims[5] = {cuuint64_t(inner * w), cuuint64_t(rlo), cuuint64_t(rhi), cuuint64_t(n2), cuuint64_t(n1)};
-  cuuint64_t strides[4] = {cuuint64_t(si * int64_t(esz)), cuuint64_t(rlo * si * int64_t(esz)),
+  cuuint64_t strides[4] = {cuuint64_t(si * int64_t(esz)),
+                           cuuint64_t((si_hi ? si_hi : rlo * si) * int64_t(esz)),
                            cuuint64_t(s2 * int64_t(esz)), cuuint64_t(s1 * int64_t(esz))};
   for (int k = 0; k < 4; ++k)
     if (strides[k] % 16 || strides[k] >= (cuuint64_t(1) << 40)) {

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(128) tma_copy(const __grid_constant__ CUtensor
 template <int W, int NB>
 __global__ void __launch_bounds__(128) tma_copy3(const __grid_constant__ CUtensorMap in,
                                                  const __grid_constant__ CUtensorMap out, int ntiles, int ncolt,
-                                                 int n1s, int order) {
+                                                 int n1s, int order, int blk) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NB * W * 256);
   const int gs = gridDim.x;
@@ -99,9 +99,16 @@ __global__ void __launch_bounds__(128) tma_copy3(const __grid_constant__ CUtenso
         : "memory");
     int c, n1, ib;
     coords(t, c, n1, ib);
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&out),
-                 "r"(su(sm + s * W * 256)), "r"(c), "r"(n1), "r"(ib)
-                 : "memory");
+    if (blk) {
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                       &out),
+                   "r"(su(sm + s * W * 256)), "r"(c), "r"(n1 % blk), "r"(ib), "r"(n1 / blk)
+                   : "memory");
+    } else {
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&out),
+                   "r"(su(sm + s * W * 256)), "r"(c), "r"(n1), "r"(ib)
+                   : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;");
     if (t + NB * gs < ntiles) {
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -114,18 +121,27 @@ __global__ void __launch_bounds__(128) tma_copy3(const __grid_constant__ CUtenso
 static PFN_cuTensorMapEncodeTiled_v12000 enc();
 
 template <int W, int NB>
-static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int order = 0) {
+static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int order = 0, int blk = 0) {
   CUtensorMap mi, mo;
   const size_t n2 = rows / n1s;
   cuuint64_t dims[3] = {256, cuuint64_t(n1s), n2};
   cuuint64_t str[2] = {2048, cuuint64_t(n1s) * 2048};
   cuuint32_t box[3] = {W / 8, 1, 256};
-  cuuint32_t es[3] = {1, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
   auto f = enc();
   f(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, a, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, b, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (blk) {
+    // blocked output: logical (n1, i) at row ((n1/blk)*n2 + i)*blk + n1%blk
+    cuuint64_t d4[4] = {256, cuuint64_t(blk), n2, cuuint64_t(n1s / blk)};
+    cuuint64_t s4[3] = {2048, cuuint64_t(blk) * 2048, cuuint64_t(blk) * n2 * 2048};
+    cuuint32_t b4[4] = {W / 8, 1, 256, 1};
+    f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, b, d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, b, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   const int ncolt = 2048 / W;
   const int ntiles = int(n2 / 256) * n1s * ncolt;
   const size_t smem = size_t(NB) * W * 256 + 64;
@@ -134,15 +150,15 @@ static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int 
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order);
+  tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order, blk);
   cudaEventRecord(e0);
-  for (int k = 0; k < 3; ++k) tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order);
+  for (int k = 0; k < 3; ++k) tma_copy3<W, NB><<<grid, 128, smem>>>(mi, mo, ntiles, ncolt, n1s, order, blk);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  printf("strided TMA box %4d B x 256 rows, row stride %8zu KB, order %d, ring %d, %d CTA/SM: %7.1f GB/s  (%s)\n", W,
-         size_t(n1s) * 2, order, NB, blocks_per_sm, 2.0 * double(n2 / 256 * 256) * n1s * 2048 * 3 / (ms / 1e3) / 1e9,
+  printf("strided TMA box %4d B x 256 rows, row stride %8zu KB, order %d, out block %d, ring %d, %d CTA/SM: %7.1f GB/s  (%s)\n", W,
+         size_t(n1s) * 2, order, blk, NB, blocks_per_sm, 2.0 * double(n2 / 256 * 256) * n1s * 2048 * 3 / (ms / 1e3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -207,8 +223,9 @@ int main() {
   // strided rows (four-step passes): 64-byte rows at 2 KB .. 4 MB stride
   for (int n1s : {1, 8, 256, 2048}) run3<64, 4>(a, b, rows, n1s, 2);
   for (int n1s : {1, 256, 2048}) run3<128, 4>(a, b, rows, n1s, 2);
-  // padded strides: 4 MB + 2 KB * (n1s - 2048)
-  for (int n1s : {2049, 2064, 2080, 2112, 2304, 3072}) run3<64, 4>(a, b, rows - rows % n1s, n1s, 2);
+  // 4 MB-strided input, blocked (128 KB-strided) output
+  run3<64, 4>(a, b, rows, 2048, 2, 0, 64);
+  run3<64, 4>(a, b, rows, 256, 2, 0, 64);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
