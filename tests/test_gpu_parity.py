@@ -222,6 +222,33 @@ def test_convolution_plan_shapes():
         _close(op.backward(x.astype(np.complex64)), orc.apply(ref, x, 1), 1e-5, f"C{n} c64 bwd")
 
 
+def test_lowrank_shapes():
+    """Rank-r factors U diag(s) V^H against Product(Dense(U), Dense(diag(s) V^H))
+    (the reference vehicle, leaves.py:40-46): ranks below / at the 32 limit,
+    column counts that are not multiples of the 128-column tiles, row counts
+    that are not multiples of the row chunks, with and without s, both
+    precisions, forward and adjoint, accumulate (inside a Sum)."""
+    rng = np.random.default_rng(33)
+    for n, m, r, K in ((1000, 777, 5, 3), (4099, 130, 17, 130), (65, 2000, 32, 200), (3000, 3000, 32, 128)):
+        U = (rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))) / np.sqrt(n)
+        V = (rng.standard_normal((m, r)) + 1j * rng.standard_normal((m, r))) / np.sqrt(m)
+        s = rng.standard_normal(r) + 1j * rng.standard_normal(r)
+        for with_s in (False, True):
+            op = sm.LowRank(U, V, s) if with_s else sm.LowRank(U, V)
+            Vs = V * np.conj(s)[None, :] if with_s else V
+            ref = orc.product(orc.dense(U), orc.dense(Vs.conj().T))
+            x = rng.standard_normal((m, K)) + 1j * rng.standard_normal((m, K))
+            y = rng.standard_normal((n, K)) + 1j * rng.standard_normal((n, K))
+            _close(op.forward(x), orc.apply(ref, x), 1e-12, f"LR {n}x{m} r{r} K{K} s{with_s} fwd")
+            _close(op.backward(y), orc.apply(ref, y, 1), 1e-12, f"LR {n}x{m} r{r} K{K} s{with_s} bwd")
+            _close(op.forward(x.astype(np.complex64)), orc.apply(ref, x), 1e-5, f"LR c64 {n}x{m} r{r}")
+        if n == m:
+            tot = sm.Sum(sm.Diag(np.ones(n)), sm.LowRank(U, V))
+            x = rng.standard_normal((n, K)) + 1j * rng.standard_normal((n, K))
+            _close(tot.forward(x), x + orc.apply(orc.product(orc.dense(U), orc.dense(V.conj().T)), x), 1e-12,
+                   f"Sum+LR {n} acc")
+
+
 def test_adjoint_identity_random_ops():
     rng = np.random.default_rng(5)
     ops = [sm.Fourier(1000), sm.Circulant(rng.standard_normal(5000)),
