@@ -132,6 +132,13 @@ struct Ctx {
     note("lowrank_expand");
     if (!measure) launch_lowrank_expand(dt, a, device, stream, false);
   }
+
+  // Fork / join with the device's side stream (independent branches of a
+  // node run concurrently; graph-capturable event edges).  Disabled in
+  // measure and profiling mode (the per-launch profile needs one timeline).
+  bool can_fork() const { return !measure && !prof; }
+  cudaStream_t fork();               // side stream, ordered after this stream
+  void join(cudaStream_t side);      // this stream waits for the side stream
 };
 
 // A device array owned by a plan.
