@@ -1,19 +1,21 @@
 // tile_tma.cuh — persistent, TMA-fed FFT tile pass.
 //
-// Same math as fft_tile_kernel's fast variant (tile_impl.cuh), restructured for
-// HBM throughput on sm_100a:
-//   * persistent CTAs (two per SM) walk over tiles of CT columns x N rows;
+// Same math as fft_tile_kernel (tile_impl.cuh), restructured for HBM
+// throughput on sm_100a:
+//   * persistent CTAs (as many per SM as shared memory allows, up to 4) walk
+//     round-robin over tiles of CT columns x N rows;
 //   * one elected thread loads a whole tile with a single 5-D TMA box
-//     (cp.async.bulk.tensor) into a dense shared buffer, tracked by an
-//     mbarrier — no load instructions, addresses or registers in the math warps;
-//   * the landing buffer doubles as the exchange buffer (rows permuted as
-//     row ^ ((row >> 4) & (X-1)) to stay bank-conflict free), so a CTA needs
-//     one tile of shared memory plus its twiddle table and two CTAs fit per SM:
-//     while one CTA shuffles and computes, the other's TMA load is in flight;
-//   * stage twiddles come from a per-CTA shared copy of W_N (quad layout in
-//     single precision: every twiddle multiply is FMUL2 + FFMA2);
-//   * four-step twiddles are looked up before the transform so their latency
-//     hides behind it; results leave straight from registers.
+//     (cp.async.bulk.tensor) into a 2-3 deep ring of landing buffers tracked by
+//     mbarriers, together with the tile's side data (spectrum slice, per-tile
+//     pre/post vector slice, four-step twiddle slice) as 1-D bulk copies on
+//     the same barrier — no load instructions or addresses in the math warps;
+//   * the landing buffer doubles as the exchange buffer (rows XOR-swizzled by
+//     the writing stage's radix, ex_row in fft_core.cuh, bank-conflict free);
+//   * stage twiddles come from a per-CTA staged table (st_twoff layout, odd
+//     lane strides; quad layout in single precision, so every twiddle multiply
+//     is FMUL2 + FFMA2);
+//   * the output tile is staged in the landing buffer and leaves with one TMA
+//     store; masked passes (zero padding / truncation) use extent-limited maps.
 #pragma once
 
 #include "tile_impl.cuh"
@@ -538,8 +540,10 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
 inline int tma_variant() {
   static int v = -1;
   if (v < 0) {
-    // 1 (default): radix-32 stages, 3-deep landing ring, one CTA per SM
-    // 3: radix-16 stages
+    // 1 (default): radix-32 stages, 3-deep landing ring for complex64 >= 1024
+    // points; 3: radix-16 stages there too.  (Measured and dropped, round 1:
+    // single-buffer two-CTA-per-SM rings, 1/2/4-column complex128 tiles and
+    // radix-8 stages for 256..1024 points — all slower.)
     const char* e = getenv("SMAT_TMA_VARIANT");
     v = e ? atoi(e) : 1;
   }
@@ -548,23 +552,8 @@ inline int tma_variant() {
 
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
-  const int v = tma_variant();
   if constexpr (N >= 1024 && sizeof(C) == 8) {
-    // 6: one buffer, two CTAs per SM;  7: same with 4-column tiles
-    if (v == 6) return fft_tma_launch_v<C, N, 32, 1>(a, s);
-    if (v == 7) return fft_tma_launch_v<C, N, 32, 1, 4>(a, s);
-    if (v == 10 && a.mid) return fft_tma_launch_v<C, N, 16, 0>(a, s);  // radix-16 spectrum pass
-    if (v != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
-  }
-  if constexpr (N == 1024 && sizeof(C) == 16) {
-    if (v == 2) return fft_tma_launch_v<C, N, 16, 1>(a, s);  // 2 CTAs/SM, one buffer each
-    if (v == 8) return fft_tma_launch_v<C, N, 16, 1, 2>(a, s);  // 2 CTAs/SM of 2-column tiles
-    if (v == 11) return fft_tma_launch_v<C, N, 32, 1>(a, s);  // radix-32, 128 threads, 2 CTAs/SM
-    // radix-8 stages: 512 threads per tile, half the registers per thread
-    if (v == 5 && !a.mid) return fft_tma_launch_v<C, N, 8, 0>(a, s);
-  }
-  if constexpr (N == 2048 && sizeof(C) == 16) {
-    if (v == 9) return fft_tma_launch_v<C, N, 16, 1, 1>(a, s);  // 2 CTAs/SM of 1-column tiles
+    if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
   }
   // short transforms: radix-8 stages (palindromic lists for 64 and 128, so the
   // spectrum pass qualifies), several CTAs per SM
