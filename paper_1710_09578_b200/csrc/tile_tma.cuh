@@ -45,7 +45,11 @@ struct TmaGeom {
   static constexpr bool TVSL = TV && sizeof(C) == 16;
   static constexpr size_t TVSB = TVSL ? size_t(N) * 16 : 0;
   static constexpr size_t STAGE = BUF + SPB + TVSB;
-  static constexpr size_t TWB = size_t(N) * 16;                    // W_N (float4 quads / double2)
+  // staged stage-twiddle table(s) (float4 quads / double2): one when the stage
+  // list is a palindrome (the mirrored inverse of the spectrum pass shares it),
+  // else a second one for the mirrored list (short transforms only)
+  static constexpr bool DUAL = !st_palindrome(N, E);
+  static constexpr size_t TWB = size_t(N) * 16 * (DUAL ? 2 : 1);
   static constexpr size_t TVB = TV && !TVSL ? size_t(N) * 16 : 0;  // per-tile four-step twiddles
   // ring of landing buffers: tile t computes in one while t+1.. load into the others
   static constexpr int NBUF =
@@ -183,23 +187,30 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
   };
   if (int(blockIdx.x) < ntiles) tv_prefetch(blockIdx.x);
   // staged stage-twiddle table (st_twoff layout) from the global W_4096 table;
-  // the spectrum passes' mirrored inverse transform runs the same (palindromic)
-  // stage list and shares it
-  static_assert(!MID || st_palindrome(N, E), "spectrum pass needs a palindromic stage list");
-  for (int e = tid; e < N - R0; e += G::T) {
-    int t4096 = 0;
+  // the spectrum passes' mirrored inverse transform runs the same stage list
+  // when it is a palindrome and shares the table, else reads a second one
+  constexpr bool DUAL = MID && G::DUAL;
+  // (16-byte entries: float4 quads or double2)
+  C* tws_mir = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(tws) + (DUAL ? N * 16 : 0));
 #pragma unroll
-    for (int S = 1; S < NST; ++S) {
-      const int RS = st_radix(N, E, S, false), NS = st_ns(N, E, S, false), OFF = st_twoff(N, E, S, false);
-      if (e >= OFF && e < OFF + NS * (RS - 1)) {
-        const int k = (e - OFF) / (RS - 1), r = (e - OFF) % (RS - 1) + 1;
-        t4096 = (r * k * (4096 / (NS * RS))) & 4095;
+  for (int half = 0; half < (DUAL ? 2 : 1); ++half) {
+    const bool mir = half == 1;
+    for (int e = tid; e < N - st_radix(N, E, 0, mir); e += G::T) {
+      int t4096 = 0;
+#pragma unroll
+      for (int S = 1; S < NST; ++S) {
+        const int RS = st_radix(N, E, S, mir), NS = st_ns(N, E, S, mir), OFF = st_twoff(N, E, S, mir);
+        if (e >= OFF && e < OFF + NS * (RS - 1)) {
+          const int k = (e - OFF) / (RS - 1), r = (e - OFF) % (RS - 1) + 1;
+          t4096 = (r * k * (4096 / (NS * RS))) & 4095;
+        }
       }
-    }
-    if constexpr (sizeof(C) == 8) {
-      reinterpret_cast<float4*>(tws)[e] = __ldg(reinterpret_cast<const float4*>(p.tw) + t4096);
-    } else {
-      tws[e] = __ldg(reinterpret_cast<const C*>(p.tw) + t4096);
+      C* dst = mir ? tws_mir : tws;
+      if constexpr (sizeof(C) == 8) {
+        reinterpret_cast<float4*>(dst)[e] = __ldg(reinterpret_cast<const float4*>(p.tw) + t4096);
+      } else {
+        dst[e] = __ldg(reinterpret_cast<const C*>(p.tw) + t4096);
+      }
     }
   }
   __syncthreads();
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
             a[u * RF + r] = conj(cmul(a[u * RF + r], sv));
           }
       }
-      fft_stages<C, N, E, CT, true, 0, LAY, N, true>(a, buf, j, cs, tws);
+      fft_stages<C, N, E, CT, true, 0, LAY, N, true>(a, buf, j, cs, tws_mir);
     }
     // all exchange reads of the landing buffer are done after this barrier
     __syncthreads();
@@ -508,8 +519,6 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
     using GV = TmaGeom<C, N, EP, NB, TV, MV || KV, CTO>;
     if constexpr (GV::SMEM > 232448) {
       return false;  // does not fit one SM: per-tile kernel
-    } else if constexpr (MV && !st_palindrome(N, GV::E)) {
-      return false;  // the spectrum pass shares one staged table between its two transforms
     } else {
       if (GV::TVSL && !a.tw_slices) return false;  // needs the precomputed twiddle slices
       const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
@@ -555,10 +564,11 @@ inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
   if constexpr (N >= 1024 && sizeof(C) == 8) {
     if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
   }
-  // short transforms: radix-8 stages (palindromic lists for 64 and 128, so the
-  // spectrum pass qualifies), several CTAs per SM
-  if constexpr (N < 256) return fft_tma_launch_v<C, N, 8, 0>(a, s);
-  else return fft_tma_launch_v<C, N, 16, 0>(a, s);
+  // short transforms: several CTAs per SM; SMAT_TMA_VARIANT=8 -> radix-8 stages
+  if constexpr (N < 256) {
+    if (tma_variant() == 8) return fft_tma_launch_v<C, N, 8, 0>(a, s);
+  }
+  return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }
 
 }  // namespace smat
