@@ -222,6 +222,35 @@ def test_convolution_plan_shapes():
         _close(op.backward(x.astype(np.complex64)), orc.apply(ref, x, 1), 1e-5, f"C{n} c64 bwd")
 
 
+@pytest.mark.parametrize("K", [1, 3, 8, 64])
+def test_four_step_paths_sweep(K):
+    """Four-step transforms through every pass variant: blocked intermediate
+    (single batch) on the TMA pass (K a multiple of the tile width) and on the
+    per-tile pass (K = 1, 3), unblocked intermediates under a Kronecker batch,
+    Bluestein with Diag·Fourier·Diag folded into the chirps, both precisions."""
+    rng = np.random.default_rng(100 + K)
+
+    def cn(*shape):
+        return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+    cases = []
+    for n in (1 << 13, 1 << 15, 1 << 17):
+        c = cn(n)
+        cases.append((sm.Circulant(c), orc.circulant(c), n))
+    for n in (5003, 40_009):
+        d1, d2 = np.exp(2j * np.pi * rng.random(n)), np.exp(2j * np.pi * rng.random(n))
+        cases.append((sm.Product(sm.Diag(d1), sm.Fourier(n), sm.Diag(d2)),
+                      orc.product(orc.diagonal(d1), orc.fourier(n), orc.diagonal(d2)), n))
+    c = cn(1 << 13)
+    cases.append((sm.Kron(sm.Hadamard(1), sm.Circulant(c)),
+                  orc.kron(orc.hadamard(1), orc.circulant(c)), 1 << 14))
+    for op, ref, n in cases:
+        x = cn(n, K)
+        for dt, tol in ((np.complex128, 1e-12), (np.complex64, 1e-5)):
+            _close(op.forward(x.astype(dt)), orc.apply(ref, x), tol, f"{op!r} K{K} {dt.__name__} fwd")
+            _close(op.backward(x.astype(dt)), orc.apply(ref, x, 1), tol, f"{op!r} K{K} {dt.__name__} bwd")
+
+
 def test_lowrank_shapes():
     """Rank-r factors U diag(s) V^H against Product(Dense(U), Dense(diag(s) V^H))
     (the reference vehicle, leaves.py:40-46): ranks below / at the 32 limit,
