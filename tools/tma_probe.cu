@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(128) tma_copy3(const __grid_constant__ CUtenso
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 enc();
+static CUtensorMapL2promotion g_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 
 template <int W, int NB>
 static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int order = 0, int blk = 0) {
@@ -130,17 +131,17 @@ static void run3(void* a, void* b, size_t rows, int n1s, int blocks_per_sm, int 
   cuuint32_t es[4] = {1, 1, 1, 1};
   auto f = enc();
   f(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, a, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CU_TENSOR_MAP_SWIZZLE_NONE, g_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (blk) {
     // blocked output: logical (n1, i) at row ((n1/blk)*n2 + i)*blk + n1%blk
     cuuint64_t d4[4] = {256, cuuint64_t(blk), n2, cuuint64_t(n1s / blk)};
     cuuint64_t s4[3] = {2048, cuuint64_t(blk) * 2048, cuuint64_t(blk) * n2 * 2048};
     cuuint32_t b4[4] = {W / 8, 1, 256, 1};
     f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, b, d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CU_TENSOR_MAP_SWIZZLE_NONE, g_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     f(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, b, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CU_TENSOR_MAP_SWIZZLE_NONE, g_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   const int ncolt = 2048 / W;
   const int ntiles = int(n2 / 256) * n1s * ncolt;
@@ -223,6 +224,12 @@ int main() {
   // strided rows (four-step passes): 64-byte rows at 2 KB .. 4 MB stride
   for (int n1s : {1, 8, 256, 2048}) run3<64, 4>(a, b, rows, n1s, 2);
   for (int n1s : {1, 256, 2048}) run3<128, 4>(a, b, rows, n1s, 2);
+  // L2 promotion at the 4 MB stride
+  g_promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  run3<64, 4>(a, b, rows, 2048, 2);
+  g_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  run3<64, 4>(a, b, rows, 2048, 2);
+  g_promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   // 4 MB-strided input, blocked (128 KB-strided) output
   run3<64, 4>(a, b, rows, 2048, 2, 0, 64);
   run3<64, 4>(a, b, rows, 256, 2, 0, 64);
