@@ -428,7 +428,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.pre_gmul = N2;
     }
     a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
-    if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, false, true);
+    a.tw_slices = twiddle_slices(c.device, Nt, N2, false, dbl);
     c.fft(cdt, int(N2), a);
   } else {
     FftArgs a;
@@ -446,7 +446,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.pre_gmul = N2;
     }
     a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
-    if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, false, true);
+    a.tw_slices = twiddle_slices(c.device, Nt, N2, false, dbl);
     c.fft(cdt, int(N2), a);
   }
   if (!io.mid) {
@@ -490,7 +490,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = 1; a.mid_gmul = N1;
       if (!tw3) {
         a.tw_on = 1; a.tw_inv = 1; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
-        if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N1, true, true);
+        a.tw_slices = twiddle_slices(c.device, Nt, N1, true, dbl);
       }
       c.fft(cdt, int(N1), a);
     }
@@ -515,7 +515,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
         // pass 2's inverse twiddle W^-(n1*k2), applied to this pass's input
         a.tw_on = 1; a.tw_pre = 1; a.tw_inv = 1;
         a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
-        if (dbl) a.tw_slices = twiddle_slices(c.device, Nt, N2, true, true);
+        a.tw_slices = twiddle_slices(c.device, Nt, N2, true, dbl);
       }
       a.post = io.post; a.post_conj = io.post_conj; a.conj_y = io.conj_y;
       if (io.post_fs) {

@@ -27,7 +27,9 @@ namespace smat {
 // exchange fewer for N = 1024); NB: landing buffers per CTA (0 = as many as fit,
 // up to 3).
 // CTO: columns per tile override (0 = default).
-template <class C, int N, int EP = 16, int NB = 0, bool TV = false, bool MS = false, int CTO = 0>
+// MS: side slice in every stage — 0 none, 1 spectrum (MID pass), 2 pre/post
+// vector (masked pass).
+template <class C, int N, int EP = 16, int NB = 0, bool TV = false, int MS = 0, int CTO = 0>
 struct TmaGeom {
   static constexpr int E = N < EP ? N : EP;
   // (double-precision 2048-point tiles: two columns, so that two landing
@@ -39,10 +41,11 @@ struct TmaGeom {
   static constexpr int LAY = ROWB >= 128 ? 1 : 128 / ROWB;          // exchange row permutation
   static constexpr size_t BUF = size_t(N) * CT * sizeof(C);         // one dense TMA box
   static constexpr size_t SPB = MS ? size_t(N) * 16 : 0;           // the tile's spectrum slice
-  // four-step twiddles: double precision bulk-loads the tile's slice of a
-  // precomputed table with the tile (TVSL); single precision assembles them
-  // per CTA from the two-level table (TVB)
-  static constexpr bool TVSL = TV && sizeof(C) == 16;
+  // four-step twiddles: double precision and the single-precision spectrum
+  // pass bulk-load the tile's slice of a precomputed table with the tile
+  // (TVSL); the other single-precision twiddle passes assemble them per CTA
+  // from the two-level table (TVB), which keeps their landing rings deeper
+  static constexpr bool TVSL = TV && (sizeof(C) == 16 || MS == 1);
   static constexpr size_t TVSB = TVSL ? size_t(N) * 16 : 0;
   static constexpr size_t STAGE = BUF + SPB + TVSB;
   // staged stage-twiddle table(s) (float4 quads / double2): one when the stage
@@ -77,11 +80,11 @@ enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21 };
 // spectrum of the MID pass).  goff is uniform over a tile (launcher check), so
 // the valid counts are per tile.
 template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK, int CTO>
-__global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::T,
-                                  TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>::MINB)
+__global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 0, CTO>::T,
+                                  TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 0, CTO>::MINB)
     fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                    const FftDev p, const int ntiles, const int ein, const int eout, const int npatch) {
-  using G = TmaGeom<C, N, EP, NB, TW, MID || MSK, CTO>;
+  using G = TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 0, CTO>;
   using R = typename RealOf<C>::T;
   constexpr int E = G::E, CT = G::CT, TPC = G::TPC, LAY = G::LAY;
   constexpr int NST = st_count(N, E);
@@ -516,7 +519,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag, auto msk_tag) {
     constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value,
                    KV = decltype(msk_tag)::value;
-    using GV = TmaGeom<C, N, EP, NB, TV, MV || KV, CTO>;
+    using GV = TmaGeom<C, N, EP, NB, TV, MV ? 1 : KV ? 2 : 0, CTO>;
     if constexpr (GV::SMEM > 232448) {
       return false;  // does not fit one SM: per-tile kernel
     } else {
