@@ -41,11 +41,13 @@ struct TmaGeom {
   static constexpr int LAY = ROWB >= 128 ? 1 : 128 / ROWB;          // exchange row permutation
   static constexpr size_t BUF = size_t(N) * CT * sizeof(C);         // one dense TMA box
   static constexpr size_t SPB = MS ? size_t(N) * 16 : 0;           // the tile's spectrum slice
-  // four-step twiddles: double precision and the single-precision spectrum
-  // pass bulk-load the tile's slice of a precomputed table with the tile
-  // (TVSL); the other single-precision twiddle passes assemble them per CTA
-  // from the two-level table (TVB), which keeps their landing rings deeper
-  static constexpr bool TVSL = TV && (sizeof(C) == 16 || MS == 1);
+  // four-step twiddles: the tile's slice of a precomputed table, bulk-loaded
+  // with the tile (TVSL; measured faster than assembling them per CTA from
+  // the two-level table even where it costs a landing buffer: C2's twiddle
+  // pass 0.224 -> 0.199 ms with a two- instead of three-deep ring).  Short
+  // single-precision tiles keep the per-CTA table (TVB): C3's 64-point
+  // masked pass ran 0.053 ms that way vs 0.070 ms with slices.
+  static constexpr bool TVSL = TV && (sizeof(C) == 16 || N >= 512);
   static constexpr size_t TVSB = TVSL ? size_t(N) * 16 : 0;
   static constexpr size_t STAGE = BUF + SPB + TVSB;
   // staged stage-twiddle table(s) (float4 quads / double2): one when the stage
