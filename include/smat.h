@@ -88,7 +88,9 @@ typedef enum smat_kind {
   SMAT_ADJOINT = 13,   /* Adjoint(base)                    core.py:229-253      */
   SMAT_BLOCKDIAG = 14, /* BlockDiag(*blocks)               composites.py:196-236*/
   SMAT_BLOCKS = 15,    /* Blocks(grid)                     composites.py:124-193*/
-  SMAT_SCALED = 16     /* scalar * base (Polynomial/Power building block)       */
+  SMAT_SCALED = 16,    /* scalar * base (Polynomial/Power building block)       */
+  SMAT_SPARSE = 17,    /* Sparse(rows, cols, triplets) CSR  leaves.py:100-159   */
+  SMAT_POLYNOMIAL = 18 /* Polynomial(base, coeffs) Horner   composites.py:323-365*/
 } smat_kind;
 
 /* A host-resident parameter array (copied to the device by plan build). */
@@ -120,6 +122,11 @@ typedef struct smat_param {
  *              LOWRANK:  param[0] = U (rows x r), param[1] = V (cols x r),
  *                        param[2] = s (r) or empty
  *              PARTIAL:  param[0] = row indices (I64), param[1] = col indices
+ *              SPARSE:   param[0] = row_ptr (I64, rows+1), param[1] = col_idx
+ *                        (I64, nnz), param[2] = values (nnz), duplicates summed
+ *                        (the reference's csr_matrix.sum_duplicates)
+ *              POLYNOMIAL: one child (square base), param[0] = ascending
+ *                        coefficients (F64 or C128)
  */
 typedef struct smat_node {
   int32_t kind;
@@ -191,6 +198,58 @@ SMAT_API void smat_plan_free(smat_plan* plan);
 SMAT_API const char* smat_last_error(void);
 
 SMAT_API int smat_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident solver steps (pkg/src/linopkit/solvers.py).  Every vector is
+ * an (n, ncols) C-contiguous float64 (SMAT_F64) or complex128 (SMAT_C128)
+ * device block; `scratch` is caller device memory of at least
+ * smat_solver_scratch_bytes(n, ncols) bytes; all calls are asynchronous on
+ * `stream` and CUDA-graph capturable.  The operator applications in between
+ * are ordinary smat_apply calls.
+ * ------------------------------------------------------------------------- */
+
+/* Scratch bytes the solver steps need for (n, ncols) blocks. */
+SMAT_API size_t smat_solver_scratch_bytes(int64_t n, int64_t ncols);
+
+/* Per-column CG state: `state` is a device double[ncols][SMAT_CG_STATE] array,
+ * fields in order: rs_old, threshold, alpha, beta, iterations, status
+ * (0 running, 1 converged, 2 breakdown — non-positive curvature, 3 iteration
+ * limit reached), residual norm, curvature at breakdown. */
+#define SMAT_CG_STATE 8
+
+/* x = 0, r = p = b, rs_old = |b|^2, threshold = tol * |b| per column; a zero
+ * column is converged at iteration 0 (solvers.py:75-84). */
+SMAT_API int smat_cg_init(int32_t dtype, int64_t n, int64_t ncols, const void* b, void* x, void* r, void* p,
+                          double* state, double tol, void* scratch, size_t scratch_bytes, void* stream);
+
+/* One conjugate-gradient iteration on every running column given ap = A p
+ * (solvers.py:85-102): curvature / breakdown test, x += alpha p,
+ * r -= alpha ap, convergence test, p = r + beta p. */
+SMAT_API int smat_cg_step(int32_t dtype, int64_t n, int64_t ncols, void* x, void* r, void* p, const void* ap,
+                          double* state, int64_t max_iter, void* scratch, size_t scratch_bytes, void* stream);
+
+/* ISTA halves (solvers.py:182-192) on length-n vectors.  state = device
+ * double[2]: l1 norm of the current x, step counter k.
+ * residual: r = b - mx, trace[k] = lam * l1 + |r|^2 / 2, k += 1.
+ * update:   x = soft_threshold(x + alpha * g, level), l1 = sum |x|. */
+SMAT_API int smat_ista_residual(int32_t dtype, int64_t n, const void* b, const void* mx, void* r, double* trace,
+                                double* state, double lam, void* scratch, size_t scratch_bytes, void* stream);
+SMAT_API int smat_ista_update(int32_t dtype, int64_t n, void* x, const void* g, double alpha, double level,
+                              double* state, void* scratch, size_t scratch_bytes, void* stream);
+
+/* One power-method step given w = A v (or A^H A v) (solvers.py:318-332).
+ * state = device double[6]: estimate |v^H w|, iterations, done, converged,
+ * (internal), zero-iterate flag; v = w / |w| unless done. */
+SMAT_API int smat_power_step(int32_t dtype, int64_t n, void* v, const void* w, double* state, double tol,
+                             void* scratch, size_t scratch_bytes, void* stream);
+
+/* y = soft_threshold(x, c) elementwise (solvers.py:22-34); y may alias x. */
+SMAT_API int smat_soft_threshold(int32_t dtype, int64_t n, const void* x, void* y, double c, void* stream);
+
+/* out_index[0] = argmax_i |g[i]| over i with excluded[i] == 0 (excluded may be
+ * null), lowest index on ties — OMP's atom pick (solvers.py:233-235). */
+SMAT_API int smat_abs_argmax(int32_t dtype, int64_t n, const void* g, const unsigned char* excluded,
+                             int64_t* out_index, void* scratch, size_t scratch_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -344,3 +344,195 @@ def apply(op, x, direction: int = 0):
 def to_dense(op) -> np.ndarray:
     eye = np.eye(op[3], dtype=np.float64 if op[4] else np.complex128)
     return apply(op, eye, 0)
+
+
+# ------------------------------------------------- §8(f) operators ---------
+
+
+def sparse(rows, cols, triplets):
+    """CSR from (row, col, value) triplets, duplicates summed (leaves.py:100-159);
+    forward CSR @ x, backward conj(CSR)^T @ y, as explicit row loops."""
+    tri = list(triplets)
+    i = np.asarray([t[0] for t in tri], dtype=np.intp)
+    j = np.asarray([t[1] for t in tri], dtype=np.intp)
+    v = np.asarray([t[2] for t in tri]) if tri else np.zeros(0)
+    real = not np.iscomplexobj(v)
+    v = v.astype(np.float64 if real else np.complex128)
+
+    def fwd(x):
+        out = np.zeros((rows, x.shape[1]), dtype=np.result_type(v.dtype, x.dtype))
+        np.add.at(out, i, v[:, None] * x[j])
+        return out
+
+    def bwd(y):
+        out = np.zeros((cols, y.shape[1]), dtype=np.result_type(v.dtype, y.dtype))
+        np.add.at(out, j, np.conj(v)[:, None] * y[i])
+        return out
+
+    return (fwd, bwd, rows, cols, real)
+
+
+def polynomial(base, coeffs):
+    """sum_k coeffs[k] base^k by Horner's rule (composites.py:323-365)."""
+    c = np.asarray(coeffs)
+    c = c.astype(np.complex128 if np.iscomplexobj(c) else np.float64)
+
+    def run(x, which):
+        cc = np.conj(c) if which == 1 else c
+        out = cc[-1] * x
+        for ck in cc[-2::-1]:
+            out = base[which](out)
+            out = out + ck * x
+        return out
+
+    return (lambda x: run(x, 0), lambda y: run(y, 1), base[2], base[3], base[4] and not np.iscomplexobj(c))
+
+
+def power(base, k: int):
+    """k-fold composition (composites.py:368-398)."""
+
+    def run(x, which):
+        out = np.array(x, copy=True)
+        for _ in range(k):
+            out = base[which](out)
+        return out
+
+    return (lambda x: run(x, 0), lambda y: run(y, 1), base[2], base[3], base[4])
+
+
+# ------------------------------------------------------------ solvers ------
+# Restatements of pkg/src/linopkit/solvers.py on oracle operators (tuples).
+
+
+def soft_threshold(x, c):
+    """solvers.py:22-34."""
+    arr = np.asarray(x)
+    shrunk = np.maximum(np.abs(arr) - c, 0.0)
+    if not np.iscomplexobj(arr):
+        return np.sign(arr) * shrunk
+    scale = np.zeros_like(shrunk)
+    np.divide(shrunk, np.abs(arr), out=scale, where=arr != 0)
+    return arr * scale
+
+
+def cg_solve(op, y, max_iterations=None, tol=1e-10, assume_hermitian=False):
+    """Column-by-column CG (solvers.py:75-160): returns (X, iterations,
+    residual norms, converged); raises ArithmeticError on breakdown."""
+    rhs = np.asarray(y)
+    squeeze = rhs.ndim == 1
+    if squeeze:
+        rhs = rhs[:, None]
+    real = op[4] and not np.iscomplexobj(rhs)
+    dtype = np.float64 if real else np.complex128
+    max_iter = max_iterations or op[3]
+    if assume_hermitian:
+        A = lambda v: apply(op, v, 0)  # noqa: E731
+        b = rhs.astype(dtype)
+    else:
+        A = lambda v: apply(op, apply(op, v, 0), 1)  # noqa: E731
+        b = apply(op, rhs, 1).astype(dtype)
+    k = rhs.shape[1]
+    X = np.zeros((op[3], k), dtype=dtype)
+    its = np.zeros(k, dtype=int)
+    res = np.zeros(k)
+    conv = np.zeros(k, dtype=bool)
+    for col in range(k):
+        bc = b[:, col].copy()
+        x = np.zeros_like(bc)
+        r = bc.copy()
+        p = r.copy()
+        rs_old = np.real(np.vdot(r, r))
+        n0 = np.sqrt(rs_old)
+        if n0 == 0:
+            conv[col] = True
+            continue
+        thr = tol * n0
+        done = False
+        for it in range(1, max_iter + 1):
+            ap = A(p)
+            curv = np.real(np.vdot(p, ap))
+            if curv <= 1e-14 * np.linalg.norm(p) * np.linalg.norm(ap):
+                raise ArithmeticError(f"breakdown at iteration {it}")
+            alpha = rs_old / curv
+            x = x + alpha * p
+            r = r - alpha * ap
+            rs_new = np.real(np.vdot(r, r))
+            if np.sqrt(rs_new) <= thr:
+                its[col], res[col], conv[col], done = it, np.sqrt(rs_new), True, True
+                break
+            p = r + (rs_new / rs_old) * p
+            rs_old = rs_new
+        if not done:
+            its[col], res[col] = max_iter, np.sqrt(rs_old)
+        X[:, col] = x
+    if squeeze:
+        return X[:, 0], int(its[0]), float(res[0]), bool(conv[0])
+    return X, its, res, conv
+
+
+def power_iteration(op, mode="eigen", tol=1e-9, max_iter=1000, seed=0):
+    """solvers.py:277-333: (value, vector, iterations, converged)."""
+    rng = np.random.default_rng(seed)
+    n = op[3]
+    v = rng.standard_normal(n)
+    if not op[4]:
+        v = v + 1j * rng.standard_normal(n)
+    v = v / np.linalg.norm(v)
+    f = (lambda u: apply(op, u, 0)) if mode == "eigen" else (lambda u: apply(op, apply(op, u, 0), 1))
+    est = 0.0
+    for it in range(1, max_iter + 1):
+        w = f(v)
+        new = float(np.abs(np.vdot(v, w)))
+        nw = np.linalg.norm(w)
+        if nw == 0:
+            return 0.0, v, it, True
+        v = w / nw
+        if it > 1 and abs(new - est) <= tol * max(new, 1e-300):
+            return float(np.sqrt(new) if mode == "singular" else new), v, it, True
+        est = new
+    return float(np.sqrt(est) if mode == "singular" else est), v, max_iter, False
+
+
+def ista(op, b, lam, steps=100, step_size=None, seed=0):
+    """solvers.py:163-194: (x, objective trace, step size)."""
+    rhs = np.asarray(b)
+    alpha = step_size
+    if alpha is None:
+        alpha = 1.0 / (1.01 * power_iteration(op, "singular", 1e-6, 50, seed)[0] ** 2)
+    level = lam * alpha
+    x = np.zeros(op[3], dtype=np.result_type(rhs.dtype, np.float64 if op[4] else np.complex128))
+    trace = np.empty(steps + 1)
+    for k in range(steps):
+        r = rhs - apply(op, x, 0)
+        trace[k] = lam * np.abs(x).sum() + 0.5 * np.real(np.vdot(r, r))
+        x = soft_threshold(x + alpha * apply(op, r, 1), level)
+    r = rhs - apply(op, x, 0)
+    trace[-1] = lam * np.abs(x).sum() + 0.5 * np.real(np.vdot(r, r))
+    return x, trace, float(alpha)
+
+
+def omp(op, b, sparsity, residual_tol=None):
+    """solvers.py:208-261: (support, coefficients, solution, residual norm)."""
+    rhs = np.asarray(b)
+    dtype = np.result_type(rhs.dtype, np.float64 if op[4] else np.complex128)
+    rhs = rhs.astype(dtype)
+    stop = residual_tol * np.linalg.norm(rhs) if residual_tol is not None else None
+    support = []
+    cols = np.zeros((op[2], 0), dtype=dtype)
+    coeffs = np.zeros(0, dtype=dtype)
+    residual = rhs.copy()
+    for _ in range(sparsity):
+        corr = np.abs(apply(op, residual, 1))
+        corr[support] = -1.0
+        atom = int(np.argmax(corr))
+        support.append(atom)
+        unit = np.zeros(op[3], dtype=dtype)
+        unit[atom] = 1
+        cols = np.hstack([cols, apply(op, unit, 0)[:, None]])
+        coeffs = np.linalg.lstsq(cols, rhs, rcond=None)[0]
+        residual = rhs - cols @ coeffs
+        if stop is not None and np.linalg.norm(residual) <= stop:
+            break
+    sol = np.zeros(op[3], dtype=dtype)
+    sol[support] = coeffs
+    return np.asarray(support, dtype=int), coeffs, sol, float(np.linalg.norm(residual))

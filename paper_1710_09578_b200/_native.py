@@ -29,7 +29,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libsmat.so"
 F32, F64, C64, C128, I32, I64 = range(6)
 # smat_kind
 (IDENTITY, ZERO, DIAGONAL, DENSE, HADAMARD, FOURIER, CIRCULANT, TOEPLITZ, LOWRANK,
- PRODUCT, SUM, KRON, PARTIAL, ADJOINT, BLOCKDIAG, BLOCKS, SCALED) = range(17)
+ PRODUCT, SUM, KRON, PARTIAL, ADJOINT, BLOCKDIAG, BLOCKS, SCALED, SPARSE, POLYNOMIAL) = range(19)
+CG_STATE = 8  # SMAT_CG_STATE
 
 DTYPE_CODE = {
     np.dtype(np.float32): F32,
@@ -115,6 +116,42 @@ _SIGNATURES = {
         ctypes.c_int,
     ),
     "smat_plan_free": ([ctypes.c_void_p], None),
+    # device-resident solver steps (solvers.cu)
+    "smat_solver_scratch_bytes": ([ctypes.c_int64, ctypes.c_int64], ctypes.c_size_t),
+    "smat_cg_init": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_cg_step": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_ista_residual": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_ista_update": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_power_step": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_soft_threshold": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
+    "smat_abs_argmax": (
+        [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_size_t, ctypes.c_void_p],
+        ctypes.c_int,
+    ),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -34,6 +34,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler",
     "-fvisibility=hidden",
     "--expt-relaxed-constexpr",
+    "--extended-lambda",
     f"-I{INCLUDE}",
 ]
 

@@ -64,6 +64,10 @@ size_t measure(const smat::Plan& p, int dir, int64_t ncols, int64_t* launches) {
 }
 }  // namespace
 
+namespace smat {
+void set_last_error(const std::string& m) { g_err = m; }
+}  // namespace smat
+
 extern "C" {
 
 int smat_abi_version(void) { return SMAT_ABI_VERSION; }

@@ -176,6 +176,38 @@ void launch_scatter_add(int dt, const IndexArgs& a, cudaStream_t s) {
   SMAT_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------ CSR SpMM ----
+template <class P>
+__global__ void __launch_bounds__(256) csr_kernel(const CsrArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const P* val = (const P*)a.val;
+  for (int64_t w = warp; w < a.rows * a.nb_outer; w += nwarps) {
+    const int64_t i = w % a.rows, o = w / a.rows;
+    const int64_t o2 = o % a.n2, o1 = o / a.n2;
+    const P* xb = (const P*)a.x + o1 * a.xs1 + o2 * a.xs2;
+    P* yr = (P*)a.y + o1 * a.ys1 + o2 * a.ys2 + i * a.ysi;
+    const int64_t k0 = a.ptr[i], k1 = a.ptr[i + 1];
+    for (int64_t c = lane; c < a.inner; c += 32) {
+      P acc = zval<P>();
+      for (int64_t k = k0; k < k1; ++k) acc = padd(acc, pmul(val[k], xb[a.col[k] * a.xsi + c]));
+      yr[c] = a.accumulate ? padd(yr[c], acc) : acc;
+    }
+  }
+}
+template <class P> static void csr_go(const CsrArgs& a, cudaStream_t s) {
+  int64_t warps = a.rows * a.nb_outer;
+  int64_t b = (warps + 7) / 8;
+  if (b > 148 * 32) b = 148 * 32;
+  csr_kernel<P><<<unsigned(b < 1 ? 1 : b), 256, 0, s>>>(a);
+}
+void launch_csr(int dt, const CsrArgs& a, cudaStream_t s) {
+  if (a.rows * a.nb_outer == 0 || a.inner == 0) return;
+  SMAT_DT_SWITCH(dt, csr_go, a, s)
+  SMAT_CUDA(cudaGetLastError());
+}
+
 // ----------------------------------------------------------------- GEMM ----
 // 64x64 output tile per CTA (256 threads, 4x4 per thread), K in chunks of 16
 // through shared memory; optional split-K with atomic accumulation for the

@@ -39,6 +39,23 @@ struct IndexArgs {
 void launch_gather(int dt, const IndexArgs& a, cudaStream_t s);
 void launch_scatter_add(int dt, const IndexArgs& a, cudaStream_t s);
 
+// CSR sparse times block (Sparse, leaves.py:100-159):
+//   y[o, i, c] (= | +=) sum_{k in [ptr[i], ptr[i+1])} val[k] * x[o, col[k], c]
+// one warp per (row, batch) pair, lanes over the contiguous columns.
+struct CsrArgs {
+  const int64_t* ptr = nullptr;
+  const int64_t* col = nullptr;
+  const void* val = nullptr;  // plan dtype
+  int64_t rows = 0;
+  const void* x = nullptr;
+  void* y = nullptr;
+  int64_t xs1 = 0, xs2 = 0, xsi = 0;
+  int64_t ys1 = 0, ys2 = 0, ysi = 0;
+  int64_t n2 = 1, nb_outer = 1, inner = 1;  // nb_outer = n1 * n2 batches of `inner` columns
+  int32_t accumulate = 0;
+};
+void launch_csr(int dt, const CsrArgs& a, cudaStream_t s);
+
 // Batched GEMM  Y[o] (=|+=) alpha * op(A) * X[o]
 //   A: (m x k) row-major with leading dimension lda when !adj,
 //      else op(A) = A^H where A is stored (k x m) row-major.

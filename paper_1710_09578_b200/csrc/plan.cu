@@ -1196,6 +1196,74 @@ struct ScaledNode : Node {
   }
 };
 
+// Sparse(rows, cols, triplets) (leaves.py:100-159): CSR times block forward,
+// the conjugate-transposed CSR (built once at plan time, like the reference's
+// _csr_adj) backward.
+struct SparseNode : Node {
+  DevBuf *ptr = nullptr, *col = nullptr, *val = nullptr;
+  DevBuf *aptr = nullptr, *acol = nullptr, *aval = nullptr;
+  int64_t nnz = 0;
+  std::string describe() const override {
+    return "Sparse(" + std::to_string(rows) + "x" + std::to_string(cols) + ", nnz " + std::to_string(nnz) + ")";
+  }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, adj ? rows : cols);
+    CsrArgs a;
+    a.ptr = (const int64_t*)(adj ? aptr : ptr)->p;
+    a.col = (const int64_t*)(adj ? acol : col)->p;
+    a.val = (adj ? aval : val)->p;
+    a.rows = adj ? cols : rows;
+    a.x = x.p; a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
+    a.y = y.p; a.ys1 = y.s1; a.ys2 = y.s2; a.ysi = y.si;
+    a.n2 = g.n2; a.nb_outer = g.n1 * g.n2; a.inner = g.inner;
+    a.accumulate = acc;
+    c.csr(a);
+    c.release(m0);
+  }
+};
+
+// Polynomial(base, coeffs) = sum_k coeffs[k] base^k (composites.py:323-365),
+// Horner's rule on the block: out = c_d x; out = base(out) + c_k x for k < d.
+// The backward conjugates the coefficients and applies base^H.
+struct PolynomialNode : Node {
+  Node* base = nullptr;
+  std::vector<std::complex<double>> coef;
+  std::string describe() const override {
+    return "Polynomial(" + base->describe() + ", degree " + std::to_string(coef.size() - 1) + ")";
+  }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    const int64_t n = rows;
+    Blk x = promote(c, x0, g, n);
+    const int d = int(coef.size()) - 1;
+    auto cf = [&](int k, double& re, double& im) {
+      re = coef[size_t(k)].real();
+      im = adj ? -coef[size_t(k)].imag() : coef[size_t(k)].imag();
+    };
+    double re, im;
+    cf(d, re, im);
+    if (d == 0) {
+      point_copy(c, x, y, g, n, acc, nullptr, false, false, re, im);
+      c.release(m0);
+      return;
+    }
+    Blk cur = c.alloc_blk(c.dt, g, n);
+    Blk tmp = c.alloc_blk(c.dt, g, n);
+    point_copy(c, x, cur, g, n, false, nullptr, false, false, re, im);
+    for (int k = d - 1; k >= 0; --k) {
+      // the last step lands in y directly unless y accumulates
+      Blk dst = (k == 0 && !acc) ? y : tmp;
+      base->apply(c, adj, cur, dst, g, false);
+      cf(k, re, im);
+      if (re != 0.0 || im != 0.0) point_copy(c, x, dst, g, n, true, nullptr, false, false, re, im);
+      std::swap(cur, tmp);
+    }
+    if (acc) point_copy(c, cur, y, g, n, true);
+    c.release(m0);
+  }
+};
+
 // ====================================================== plan building =====
 // Device FFT of a complex128 vector (plan-build helper: spectra, Bluestein).
 void device_fft_c128(Plan& p, int64_t n, const void* in_dev, void* out_dev) {
@@ -1522,6 +1590,65 @@ struct Builder {
         a->re = nd.dparam[0];
         a->im = nd.dparam[1];
         SMAT_CHECK(dt_complex(p.dt) || a->im == 0.0, SMAT_BAD_DTYPE, "complex scale in a real plan");
+        out = a;
+        break;
+      }
+      case SMAT_SPARSE: {
+        SMAT_CHECK(dt_int(p.dt) == false, SMAT_BAD_DTYPE, "Sparse needs a floating plan");
+        auto* a = add<SparseNode>();
+        const int64_t R = nd.rows, Cn = nd.cols;
+        SMAT_CHECK(nd.param[0].dtype == SMAT_I64 && nd.param[0].len == R + 1 && nd.param[1].dtype == SMAT_I64,
+                   SMAT_BAD_ARG, "sparse: row_ptr / col_idx must be int64 (rows+1, nnz)");
+        const int64_t* rp = (const int64_t*)nd.param[0].data;
+        const int64_t* ci = (const int64_t*)nd.param[1].data;
+        const int64_t nnz = nd.param[1].len;
+        SMAT_CHECK(nd.param[2].len == nnz && rp[0] == 0 && rp[R] == nnz, SMAT_BAD_ARG, "sparse: inconsistent CSR");
+        for (int64_t i = 0; i < R; ++i) SMAT_CHECK(rp[i] <= rp[i + 1], SMAT_BAD_ARG, "sparse: row_ptr not monotone");
+        for (int64_t k = 0; k < nnz; ++k) SMAT_CHECK(ci[k] >= 0 && ci[k] < Cn, SMAT_BAD_ARG, "sparse: column index");
+        a->nnz = nnz;
+        a->ptr = upload_param(p, nd.param[0], SMAT_I64);
+        a->col = upload_param(p, nd.param[1], SMAT_I64);
+        a->val = upload_param(p, nd.param[2], p.dt);
+        // conjugate transpose: counting sort by column, stable in the row order
+        const bool cv = dt_complex(nd.param[2].dtype);
+        auto hv = convert_host(nd.param[2], cv ? SMAT_C128 : SMAT_F64);
+        std::vector<int64_t> tp(size_t(Cn) + 1, 0);
+        std::vector<int64_t> tc(static_cast<size_t>(nnz));
+        std::vector<double> tv(size_t(nnz) * (cv ? 2 : 1));
+        for (int64_t k = 0; k < nnz; ++k) ++tp[size_t(ci[k]) + 1];
+        for (int64_t j = 0; j < Cn; ++j) tp[size_t(j) + 1] += tp[size_t(j)];
+        std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+        const double* hvd = (const double*)hv.data();
+        for (int64_t i = 0; i < R; ++i)
+          for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const int64_t q = fill[size_t(ci[k])]++;
+            tc[size_t(q)] = i;
+            if (cv) {
+              tv[size_t(2 * q)] = hvd[2 * k];
+              tv[size_t(2 * q + 1)] = -hvd[2 * k + 1];
+            } else {
+              tv[size_t(q)] = hvd[k];
+            }
+          }
+        smat_param pp{tp.data(), Cn + 1, SMAT_I64, 0}, pc{tc.data(), nnz, SMAT_I64, 0},
+            pv{tv.data(), nnz, cv ? SMAT_C128 : SMAT_F64, 0};
+        a->aptr = upload_param(p, pp, SMAT_I64);
+        a->acol = upload_param(p, pc, SMAT_I64);
+        a->aval = upload_param(p, pv, p.dt);
+        out = a;
+        break;
+      }
+      case SMAT_POLYNOMIAL: {
+        auto* a = add<PolynomialNode>();
+        a->base = child(nd, 0);
+        SMAT_CHECK(a->base->rows == a->base->cols && a->base->rows == nd.rows, SMAT_BAD_SHAPE,
+                   "polynomial base must be square");
+        SMAT_CHECK(nd.param[0].len >= 1, SMAT_BAD_ARG, "polynomial needs coefficients");
+        const bool cv = dt_complex(nd.param[0].dtype);
+        SMAT_CHECK(!cv || dt_complex(p.dt), SMAT_BAD_DTYPE, "complex coefficients in a real plan");
+        auto hc = convert_host(nd.param[0], SMAT_C128);
+        const double* h = (const double*)hc.data();
+        for (int64_t k = 0; k < nd.param[0].len; ++k) a->coef.emplace_back(h[2 * k], h[2 * k + 1]);
         out = a;
         break;
       }

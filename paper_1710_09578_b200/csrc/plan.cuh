@@ -122,6 +122,11 @@ struct Ctx {
     note("gemm");
     if (!measure) launch_gemm(dt, a, device, stream, false);
   }
+  void csr(const CsrArgs& a) {
+    ++launches;
+    note("csr");
+    if (!measure) launch_csr(dt, a, stream);
+  }
   void lr_contract(const LowRankArgs& a) {
     launches += launch_lowrank_contract(dt, a, device, stream, true);
     note("lowrank_contract");

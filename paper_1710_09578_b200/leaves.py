@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _native
 from .core import LinearOperator, ScalarField, as_field, field_of, promote_field
-from .errors import EmptyInput, OrderTooLarge
+from .errors import EmptyInput, IndexOutOfRange, OrderTooLarge
 
 MAX_HADAMARD_ORDER = 30  # leaves.py:16
 
@@ -240,3 +240,97 @@ class LowRank(LinearOperator):
 
     def _param_bytes(self):
         return self.U.nbytes + self.V.nbytes + (self.s.nbytes if self.s is not None else 0)
+
+
+class Sparse(LinearOperator):
+    """Compressed-sparse-row operator built from (row, col, value) triplets
+    (leaves.py:100-159).  Duplicate coordinates are summed; the
+    conjugate-transposed CSR is built once when the device plan is compiled, so
+    the backward transform also runs in O(nnz) (one warp per output row).
+    """
+
+    def __init__(self, rows, cols, triplets):
+        rows = int(rows)
+        cols = int(cols)
+        tri = list(triplets)
+        if tri:
+            i = np.asarray([t[0] for t in tri], dtype=np.int64)
+            j = np.asarray([t[1] for t in tri], dtype=np.int64)
+            v = np.asarray([t[2] for t in tri])
+        else:
+            i = np.zeros(0, dtype=np.int64)
+            j = np.zeros(0, dtype=np.int64)
+            v = np.zeros(0)
+        if i.size and (i.min() < 0 or i.max() >= rows or j.min() < 0 or j.max() >= cols):
+            raise IndexOutOfRange(f"triplet index outside {rows}x{cols} matrix")
+        dtype = as_field(v.dtype).dtype if v.size else np.float64
+        v = v.astype(dtype)
+        # canonical CSR: rows ascending, columns ascending within a row,
+        # duplicates summed in triplet order (csr_matrix.sum_duplicates)
+        order = np.lexsort((j, i))
+        i, j, v = i[order], j[order], v[order]
+        if i.size:
+            key = i * cols + j
+            first = np.concatenate(([True], key[1:] != key[:-1]))
+            grp = np.cumsum(first) - 1
+            vals = np.zeros(int(first.sum()), dtype=dtype)
+            np.add.at(vals, grp, v)
+            i, j, v = i[first], j[first], vals
+        self._row_ptr = np.zeros(rows + 1, dtype=np.int64)
+        np.add.at(self._row_ptr, i + 1, 1)
+        self._row_ptr = np.cumsum(self._row_ptr)
+        self._col_idx = np.ascontiguousarray(j, dtype=np.int64)
+        self._values = np.ascontiguousarray(v, dtype=dtype)
+        self._init_shape(rows, cols, field_of(self._values))
+
+    @property
+    def row_ptr(self):
+        return self._row_ptr
+
+    @property
+    def col_idx(self):
+        return self._col_idx
+
+    @property
+    def values(self):
+        return self._values
+
+    @property
+    def nnz(self):
+        return int(self._values.size)
+
+    def _smat_record(self, ser):
+        return dict(kind=_native.SPARSE, rows=self.rows, cols=self.cols,
+                    params=(self._row_ptr, self._col_idx, self._values))
+
+    def _param_bytes(self):
+        # both CSR copies, with scipy's index width (leaves.py:154-158)
+        idx = 4 if max(self.rows, self.cols, self.nnz) < 2**31 else 8
+        return 2 * (self._values.nbytes + self.nnz * idx) + (self.rows + 1 + self.cols + 1) * idx
+
+
+class Parametric(LinearOperator):
+    """Operator whose entries come from a function f(i, j) (leaves.py:290-322).
+
+    The reference evaluates f row by row on every application.  Here the
+    entries are evaluated once, when the device plan is compiled, into a
+    device-resident dense factor (the host keeps only f and the shape); the
+    applications are then dense GEMM passes.
+    """
+
+    def __init__(self, f, rows, cols, field=ScalarField.COMPLEX128):
+        self.f = f
+        self._init_shape(rows, cols, as_field(field))
+
+    def _entries(self):
+        dt = self.field.dtype
+        out = np.empty((self.rows, self.cols), dtype=dt)
+        for i in range(self.rows):
+            out[i] = np.fromiter((self.f(i, j) for j in range(self.cols)), dtype=dt, count=self.cols)
+        return out
+
+    def _smat_record(self, ser):
+        return dict(kind=_native.DENSE, rows=self.rows, cols=self.cols, params=(self._entries(),))
+
+    def _param_bytes(self):
+        return 24  # function reference plus the two dimensions

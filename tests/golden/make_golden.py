@@ -26,8 +26,10 @@ HERE = Path(__file__).resolve().parent
 REPO = HERE.parent.parent
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(HERE))
 
 import linopkit as lk  # noqa: E402  (the reference)
+from make_problems import solver_problems  # noqa: E402
 
 
 def cn(rng, shape):
@@ -138,6 +140,72 @@ def gen_ops():
     return out
 
 
+def gen_extra():
+    """Sparse / Polynomial / Power operators and the solvers."""
+    P = solver_problems()
+    out = {}
+    for name in ("sparse_r", "sparse_c"):
+        q = P[name]
+        op = lk.Sparse(40, 30, list(zip(q["i"].tolist(), q["j"].tolist(), q["v"].tolist())))
+        out[f"{name}/fwd"] = op.forward(q["x"])
+        out[f"{name}/bwd"] = op.backward(q["y"])
+        out[f"{name}/nnz"] = np.asarray(op.nnz)
+        out[f"{name}/footprint"] = np.asarray(op.footprint_bytes())
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((64, 2))
+    xc = cn(rng, (16, 2))
+    c = P["poly_c"]
+    out["poly_r/x"], out["poly_c/x"] = x, xc
+    pr = lk.Polynomial(lk.Circulant(c), [0.5, -1.0, 0.25])
+    pc = lk.Polynomial(lk.Fourier(16), np.array([1.0, 0.5j, -0.25]))
+    out["poly_r/fwd"], out["poly_r/bwd"] = pr.forward(x), pr.backward(x)
+    out["poly_c/fwd"], out["poly_c/bwd"] = pc.forward(xc), pc.backward(xc)
+    pw = lk.Power(lk.Circulant(c), 3)
+    out["pow3/fwd"], out["pow3/bwd"] = pw.forward(x), pw.backward(x)
+    pf = lk.Power(lk.Fourier(16), 2)
+    out["powf/fwd"], out["powf/bwd"] = pf.forward(xc), pf.backward(xc)
+    out["pow0/fwd"] = lk.Power(lk.Hadamard(6), 0).forward(x)
+    # CG: SPD circulant (hermitian mode), complex HPD circulant, Toeplitz normal equations
+    r = lk.cg_solve(lk.Circulant(P["spd_c"]), P["cg_rhs"], lk.SolveOptions(assume_hermitian=True))
+    out["cg_spd/x"], out["cg_spd/it"], out["cg_spd/res"], out["cg_spd/conv"] = (
+        r.solution, r.iterations, r.residual_norm, r.converged)
+    r = lk.cg_solve(lk.Circulant(P["hpd_c"]), P["cg_rhs_c"], lk.SolveOptions(assume_hermitian=True))
+    out["cg_hpd/x"], out["cg_hpd/it"], out["cg_hpd/res"], out["cg_hpd/conv"] = (
+        r.solution, r.iterations, r.residual_norm, r.converged)
+    T = lk.Toeplitz(P["toe_col"], P["toe_row"])
+    r = lk.cg_solve(T, P["cg_rhs_t"])
+    out["cg_ne/x"], out["cg_ne/it"], out["cg_ne/res"], out["cg_ne/conv"] = (
+        r.solution, r.iterations, r.residual_norm, r.converged)
+    r = lk.cg_solve(T, P["cg_rhs_t"][:, 0], lk.SolveOptions(max_iterations=3))
+    out["cg_lim/x"], out["cg_lim/it"], out["cg_lim/res"], out["cg_lim/conv"] = (
+        r.solution, r.iterations, r.residual_norm, r.converged)
+    # power iteration
+    sp = lk.power_iteration(lk.Circulant(P["spd_c"]), seed=3)
+    out["pw_eig/value"], out["pw_eig/vec"], out["pw_eig/it"], out["pw_eig/conv"] = (
+        sp.value, sp.vector, sp.iterations, sp.converged)
+    sp = lk.power_iteration(T, mode="singular", tol=1e-8, seed=1)
+    out["pw_sv/value"], out["pw_sv/vec"], out["pw_sv/it"], out["pw_sv/conv"] = (
+        sp.value, sp.vector, sp.iterations, sp.converged)
+    # ISTA / OMP on compressed-sensing operators
+    Mh = lk.Partial(lk.Hadamard(7), row_indices=P["cs_rows_h"])
+    bh = Mh.forward(P["cs_x_h"])
+    res = lk.ista(Mh, bh, lk.IstaOptions(lam=0.05, steps=60))
+    out["ista_h/x"], out["ista_h/trace"], out["ista_h/alpha"] = res.solution, res.objective_trace, res.step_size
+    Mf = lk.Partial(lk.Fourier(64), row_indices=P["cs_rows_f"])
+    bf = Mf.forward(P["cs_x_f"])
+    res = lk.ista(Mf, bf, lk.IstaOptions(lam=0.02, steps=40, step_size=1.0 / 64))
+    out["ista_f/x"], out["ista_f/trace"], out["ista_f/alpha"] = res.solution, res.objective_trace, res.step_size
+    o = lk.omp(Mh, bh, 4)
+    out["omp_h/support"], out["omp_h/coef"], out["omp_h/x"], out["omp_h/res"] = (
+        o.support, o.coefficients, o.solution, o.residual_norm)
+    o = lk.omp(Mf, bf, 6, residual_tol=1e-9)
+    out["omp_f/support"], out["omp_f/coef"], out["omp_f/x"], out["omp_f/res"] = (
+        o.support, o.coefficients, o.solution, o.residual_norm)
+    out["soft_r"] = lk.soft_threshold(P["soft_r"], 0.5)
+    out["soft_c"] = lk.soft_threshold(P["soft_c"], 0.5)
+    return out
+
+
 def config_check(path):
     """Reference vs oracle on column samples of the full-size configs."""
     from oracle import linop_oracle as orc
@@ -187,7 +255,8 @@ if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
     np.savez_compressed(HERE / "kernels.npz", **gen_kernels())
     np.savez_compressed(HERE / "ops.npz", **gen_ops())
-    for f in ("kernels.npz", "ops.npz"):
+    np.savez_compressed(HERE / "extra.npz", **gen_extra())
+    for f in ("kernels.npz", "ops.npz", "extra.npz"):
         print(f, (HERE / f).stat().st_size, "bytes")
     if "--config-check" in sys.argv:
         config_check(HERE / "config_check.txt")

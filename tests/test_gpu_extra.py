@@ -1,0 +1,162 @@
+"""Device parity for the SURVEY.md §8(f) rows: Sparse (CSR kernel), Polynomial
+(native Horner node), Power, Parametric, and the device-resident solvers
+(csrc/solvers.cu + plans) against fixtures from the REAL reference
+(tests/golden/extra.npz) and the CPU oracle.
+
+Tolerances: operators relative L2 <= 1e-12 (float64 / complex128, the north
+star's bound).  Iterative solvers: the reduction order differs from numpy's,
+so iterates agree to the convergence level, not to 1e-12: solutions and
+objective traces <= 1e-9 relative, iteration counts within 2 for the
+normal-equation case (condition number squared), exact otherwise.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1710_09578_b200 as sm
+from conftest import GOLDEN, rel_l2
+from oracle import linop_oracle as orc
+
+sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+from make_problems import solver_problems  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    return dict(np.load(GOLDEN / "extra.npz"))
+
+
+@pytest.fixture(scope="module")
+def P():
+    return solver_problems()
+
+
+def test_sparse_device(G, P):
+    for name in ("sparse_r", "sparse_c"):
+        q = P[name]
+        op = sm.Sparse(40, 30, list(zip(q["i"].tolist(), q["j"].tolist(), q["v"].tolist())))
+        assert rel_l2(op.forward(q["x"]), G[f"{name}/fwd"]) < 1e-12
+        assert rel_l2(op.backward(q["y"]), G[f"{name}/bwd"]) < 1e-12
+    # a larger random CSR against the oracle, composed inside a Product
+    rng = np.random.default_rng(7)
+    tri = list(zip(rng.integers(0, 5000, 40000).tolist(), rng.integers(0, 3000, 40000).tolist(),
+                   rng.standard_normal(40000).tolist()))
+    S = sm.Sparse(5000, 3000, tri)
+    op = sm.Product(sm.Diag(rng.standard_normal(5000)), S)
+    oo = orc.product(orc.diagonal(op.factors[0].d), orc.sparse(5000, 3000, tri))
+    x = rng.standard_normal((3000, 8))
+    y = rng.standard_normal((5000, 8))
+    assert rel_l2(op.forward(x), orc.apply(oo, x, 0)) < 1e-12
+    assert rel_l2(op.backward(y), orc.apply(oo, y, 1)) < 1e-12
+    # single precision plan
+    xs = x.astype(np.float32)
+    assert rel_l2(S.forward(xs), orc.apply(orc.sparse(5000, 3000, tri), x, 0)) < 1e-5
+
+
+def test_polynomial_power_device(G, P):
+    c = P["poly_c"]
+    x, xc = G["poly_r/x"], G["poly_c/x"]
+    pr = sm.Polynomial(sm.Circulant(c), [0.5, -1.0, 0.25])
+    assert rel_l2(pr.forward(x), G["poly_r/fwd"]) < 1e-12
+    assert rel_l2(pr.backward(x), G["poly_r/bwd"]) < 1e-12
+    pc = sm.Polynomial(sm.Fourier(16), np.array([1.0, 0.5j, -0.25]))
+    assert rel_l2(pc.forward(xc), G["poly_c/fwd"]) < 1e-12
+    assert rel_l2(pc.backward(xc), G["poly_c/bwd"]) < 1e-12
+    pw = sm.Power(sm.Circulant(c), 3)
+    assert rel_l2(pw.forward(x), G["pow3/fwd"]) < 1e-12
+    assert rel_l2(pw.backward(x), G["pow3/bwd"]) < 1e-12
+    pf = sm.Power(sm.Fourier(16), 2)
+    assert rel_l2(pf.forward(xc), G["powf/fwd"]) < 1e-12
+    assert rel_l2(pf.backward(xc), G["powf/bwd"]) < 1e-12
+    assert np.array_equal(sm.Power(sm.Hadamard(6), 0).forward(x), G["pow0/fwd"])
+    # polynomial inside a Sum (accumulating path) and a degree-0 polynomial
+    s = sm.Sum(sm.Polynomial(sm.Hadamard(6), [2.0, 0.0, 1.0]), sm.Identity(64))
+    o = orc.sum_(orc.polynomial(orc.hadamard(6), [2.0, 0.0, 1.0]), orc.identity(64))
+    assert rel_l2(s.forward(x), orc.apply(o, x, 0)) < 1e-12
+    assert rel_l2(sm.Polynomial(sm.Hadamard(6), [3.0]).forward(x), 3.0 * x) < 1e-15
+    # Parametric: entries evaluated once into a device dense factor
+    f = lambda i, j: np.cos(0.1 * i * j) + 1j * np.sin(0.05 * (i - j))  # noqa: E731
+    par = sm.Parametric(f, 12, 9)
+    dense = np.array([[f(i, j) for j in range(9)] for i in range(12)])
+    xx = xc[:9]
+    assert rel_l2(par.forward(xx), dense @ xx) < 1e-12
+    assert rel_l2(par.backward(xc[:12]), dense.conj().T @ xc[:12]) < 1e-12
+
+
+def test_cg_device(G, P):
+    r = sm.cg_solve(sm.Circulant(P["spd_c"]), P["cg_rhs"], sm.SolveOptions(assume_hermitian=True))
+    assert rel_l2(r.solution, G["cg_spd/x"]) < 1e-9
+    assert np.array_equal(r.iterations, G["cg_spd/it"]) and r.converged.all()
+    assert np.allclose(r.residual_norm, G["cg_spd/res"], rtol=1e-3, atol=0)
+    r = sm.cg_solve(sm.Circulant(P["hpd_c"]), P["cg_rhs_c"], sm.SolveOptions(assume_hermitian=True))
+    assert rel_l2(r.solution, G["cg_hpd/x"]) < 1e-9 and np.array_equal(r.iterations, G["cg_hpd/it"])
+    T = sm.Toeplitz(P["toe_col"], P["toe_row"])
+    r = sm.cg_solve(T, P["cg_rhs_t"])
+    assert rel_l2(r.solution, G["cg_ne/x"]) < 1e-9
+    assert np.max(np.abs(r.iterations - G["cg_ne/it"])) <= 2 and r.converged.all()
+    r = sm.cg_solve(T, P["cg_rhs_t"][:, 0], sm.SolveOptions(max_iterations=3))
+    assert r.iterations == 3 and r.converged is False
+    assert rel_l2(r.solution, G["cg_lim/x"]) < 1e-10
+    assert abs(r.residual_norm - float(G["cg_lim/res"])) < 1e-9 * float(G["cg_lim/res"])
+    # zero right-hand side column: 0 iterations, converged (solvers.py:81-82)
+    rhs = P["cg_rhs"].copy()
+    rhs[:, 1] = 0
+    r = sm.cg_solve(sm.Circulant(P["spd_c"]), rhs, sm.SolveOptions(assume_hermitian=True))
+    assert r.iterations[1] == 0 and r.converged[1] and not np.any(r.solution[:, 1])
+    # breakdown on an indefinite operator
+    with pytest.raises(sm.BreakdownError):
+        sm.cg_solve(sm.Diag(np.array([1.0, -1.0, 2.0, 3.0])), np.array([1.0, 1.0, 0.0, 0.0]),
+                    sm.SolveOptions(assume_hermitian=True))
+
+
+def test_cg_device_eager_matches_graph(P, monkeypatch):
+    A = sm.Circulant(P["spd_c"])
+    r1 = sm.cg_solve(A, P["cg_rhs"], sm.SolveOptions(assume_hermitian=True))
+    monkeypatch.setenv("SMAT_SOLVER_GRAPHS", "0")
+    r2 = sm.cg_solve(A, P["cg_rhs"], sm.SolveOptions(assume_hermitian=True))
+    assert np.array_equal(r1.solution, r2.solution) and np.array_equal(r1.iterations, r2.iterations)
+
+
+def test_power_ista_omp_device(G, P):
+    sp = sm.power_iteration(sm.Circulant(P["spd_c"]), seed=3)
+    assert abs(sp.value - float(G["pw_eig/value"])) < 1e-9 * sp.value and sp.converged
+    assert abs(sp.iterations - int(G["pw_eig/it"])) <= 2
+    T = sm.Toeplitz(P["toe_col"], P["toe_row"])
+    sp = sm.power_iteration(T, mode="singular", tol=1e-8, seed=1)
+    assert abs(sp.value - float(G["pw_sv/value"])) < 1e-8 * sp.value
+    assert abs(sp.iterations - int(G["pw_sv/it"])) <= 3
+    Mh = sm.Partial(sm.Hadamard(7), row_indices=P["cs_rows_h"])
+    bh = Mh.forward(P["cs_x_h"])
+    res = sm.ista(Mh, bh, sm.IstaOptions(lam=0.05, steps=60))
+    assert abs(res.step_size - float(G["ista_h/alpha"])) < 1e-8 * res.step_size
+    assert rel_l2(res.solution, G["ista_h/x"]) < 1e-7 and rel_l2(res.objective_trace, G["ista_h/trace"]) < 1e-7
+    Mf = sm.Partial(sm.Fourier(64), row_indices=P["cs_rows_f"])
+    bf = Mf.forward(P["cs_x_f"])
+    res = sm.ista(Mf, bf, sm.IstaOptions(lam=0.02, steps=40, step_size=1.0 / 64))
+    assert rel_l2(res.solution, G["ista_f/x"]) < 1e-9 and rel_l2(res.objective_trace, G["ista_f/trace"]) < 1e-9
+    o = sm.omp(Mh, bh, 4)
+    assert np.array_equal(o.support, G["omp_h/support"]) and rel_l2(o.solution, G["omp_h/x"]) < 1e-9
+    o = sm.omp(Mf, bf, 6, residual_tol=1e-9)
+    assert np.array_equal(o.support, G["omp_f/support"]) and rel_l2(o.coefficients, G["omp_f/coef"]) < 1e-9
+    assert np.array_equal(sm.soft_threshold(P["soft_r"], 0.5), G["soft_r"])
+    assert rel_l2(sm.soft_threshold(P["soft_c"], 0.5), G["soft_c"]) < 1e-15
+
+
+def test_solvers_on_device_tensors(P):
+    import torch
+
+    A = sm.Circulant(P["spd_c"])
+    rhs = torch.from_numpy(P["cg_rhs"]).cuda()
+    r = sm.cg_solve(A, rhs, sm.SolveOptions(assume_hermitian=True))
+    assert r.solution.is_cuda
+    ref = orc.cg_solve(orc.circulant(P["spd_c"]), P["cg_rhs"], assume_hermitian=True)[0]
+    assert rel_l2(r.solution.cpu().numpy(), ref) < 1e-9
+    t = sm.soft_threshold(rhs, 0.3)
+    assert t.is_cuda and rel_l2(t.cpu().numpy(), orc.soft_threshold(P["cg_rhs"], 0.3)) < 1e-15
