@@ -60,7 +60,17 @@ size_t measure(const smat::Plan& p, int dir, int64_t ncols, int64_t* launches) {
   static char dummy;
   smat::run_plan(p, c, dir, &dummy, p.dt, &dummy, ncols);
   if (launches) *launches = c.launches;
-  return c.peak;
+  size_t peak = c.peak;
+  if (smat::dt_complex(p.dt)) {
+    // a real input to a complex plan may need a promoted copy first
+    smat::Ctx r;
+    r.device = p.device;
+    r.dt = p.dt;
+    r.measure = true;
+    smat::run_plan(p, r, dir, &dummy, smat::dt_real_of(p.dt), &dummy, ncols);
+    if (r.peak > peak) peak = r.peak;
+  }
+  return peak;
 }
 }  // namespace
 

@@ -97,6 +97,10 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+# how the last solver loop ran: "graph" (captured once, replayed) or "eager"
+last_loop_mode = None
+
+
 def _graphs_enabled() -> bool:
     return os.environ.get("SMAT_SOLVER_GRAPHS", "1") != "0"
 
@@ -131,6 +135,8 @@ class _Loop:
                 torch.cuda.current_stream().wait_stream(s)
                 torch.cuda.synchronize()
                 self.graph = None
+        global last_loop_mode
+        last_loop_mode = "graph" if self.graph is not None else "eager"
         for _ in range(count):
             if self.graph is not None:
                 self.graph.replay()

@@ -118,9 +118,13 @@ def test_cg_device(G, P):
 
 def test_cg_device_eager_matches_graph(P, monkeypatch):
     A = sm.Circulant(P["spd_c"])
+    from paper_1710_09578_b200 import solvers
+
     r1 = sm.cg_solve(A, P["cg_rhs"], sm.SolveOptions(assume_hermitian=True))
+    assert solvers.last_loop_mode == "graph"  # the iteration was captured and replayed
     monkeypatch.setenv("SMAT_SOLVER_GRAPHS", "0")
     r2 = sm.cg_solve(A, P["cg_rhs"], sm.SolveOptions(assume_hermitian=True))
+    assert solvers.last_loop_mode == "eager"
     assert np.array_equal(r1.solution, r2.solution) and np.array_equal(r1.iterations, r2.iterations)
 
 
