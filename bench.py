@@ -51,7 +51,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -396,6 +396,17 @@ def run_native(args, cfg):
                     "bytes_per_launch": pb, "avg_launch_ms": dom_avg_ms,
                     "share_of_step": dom_t / total if total else None,
                     "peak_source": peak_src}
+    if cfg == 3:
+        # FP32-bound config: algorithmic FFT flops of the
+        # length-8192 embedding with real-pair packing, whole step, against the
+        # nominal FP32 FFMA peak
+        flops = 2 * configs.c3_flops_per_direction(K)
+        achieved = flops / (ms_step / 1e3) / 1e12
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        roofline = {"bound": "fp32", "kernel": "all fft_c64 passes of the step", "variants": sorted(by_kernel),
+                    "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                    "traffic": None, "flops_per_step": flops,
+                    "peak_source": "nominal FP32 FFMA: 148 SMs x 128 lanes x 2 flops x 1965 MHz"}
     alg = configs.algorithmic_bytes(cfg, K)
     transform_gbs = 2 * alg / (ms_step / 1e3) / 1e9
 
@@ -457,12 +468,101 @@ def run_native(args, cfg):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------- solver leg ----
+def run_solver(args):
+    """--workload cg: conjugate gradients on the normal equations of C2's
+    operator (Circulant 2^20, 64 right-hand sides, complex128 as the
+    reference's cg_solve computes), fixed iteration count.  One step = one CG
+    iteration over all 64 columns: A p and A^H (A p) through the compiled plan
+    plus the fused step kernels, replayed from a CUDA graph."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1710_09578_b200 as sm
+    from paper_1710_09578_b200 import configs, solvers
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    w = configs.make(2)
+    op = sm.Circulant(w.params["c"])
+    K = w.ncols
+    rhs = torch.from_numpy(np.ascontiguousarray(w.X)).to(f"cuda:{dev}").to(torch.complex128)
+    del w.X
+    opts_w = sm.SolveOptions(max_iterations=args.warmup, relative_tolerance=1e-300)
+    sm.cg_solve(op, rhs, opts_w)  # warm-up: plans, workspaces, graph capture path
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    opts = sm.SolveOptions(max_iterations=args.steps, relative_tolerance=1e-300)
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        rep = sm.cg_solve(op, rhs, opts)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=f"cuda:{dev}", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_it = float(t.item()) / args.steps
+    n = 1 << 20
+    e = 16
+    # per iteration: two 3-pass c128 convolutions (read+write of the block per
+    # pass + spectrum) and the step kernels (p.ap reduce 2 blocks, x/r update
+    # 4 read + 2 write, p update 2 read + 1 write)
+    conv = 3 * 2 * n * K * e + n * e
+    step_bytes = (2 + 6 + 3) * n * K * e
+    it_bytes = 2 * conv + step_bytes
+    peak, peak_src = _peaks()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import linop_oracle as orc
+
+        its = 4
+        t0 = time.perf_counter()
+        orc.cg_solve(orc.circulant(configs.make(2, ncols=1).params["c"]), np.asarray(rhs[:, :1].cpu()),
+                     max_iterations=its, tol=1e-300)
+        dt = time.perf_counter() - t0
+        cpu = {"value": its / dt, "unit": "column-iterations/s", "cores": 1, "kind": "port",
+               "sample": f"1 of {K} columns, {its} iterations, numpy oracle of solvers.py:75-106 ({dt:.2f} s)"}
+    if rank == 0:
+        line = {
+            "metric": "CG column-iterations/s (normal equations)", "value": world * K / (ms_it / 1e3),
+            "unit": "column-iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_it, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (seeded numpy, C2 operator and block, SURVEY.md §8d)",
+            "config": {"workload": "cg_solve(Circulant(2^20), 2^20x64 complex128, normal equations)",
+                       "step": "one CG iteration over all 64 columns (A p, A^H A p, fused step kernels)",
+                       "l2": "inputs larger than L2", "graph": solvers.last_loop_mode},
+            "roofline": {"bound": "hbm", "kernel": "whole iteration", "achieved": it_bytes / (ms_it / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": it_bytes / (ms_it / 1e3) / 1e9 / peak,
+                         "traffic": None, "bytes_per_launch": it_bytes, "peak_source": peak_src},
+            "iterations_run": int(np.max(rep.iterations)),
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def w_dtype(cfg):
     return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
 
 
 def main():
     args = _args()
+    if args.workload == "cg":
+        run_solver(args)
+        return
     cfg = int(args.workload[1])
     if args.impl == "reference":
         run_reference(args, cfg)

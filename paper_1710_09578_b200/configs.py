@@ -120,6 +120,15 @@ def operator(cfg: int, w: Workload):
     raise ValueError(cfg)
 
 
+def c3_flops_per_direction(ncols: int) -> float:
+    """~0.56 M FP32 flops per column of C3 with real-pair
+    packing — two length-8192 complex FFTs (5 L log2 L each) and the spectrum
+    multiply (6 L) per packed column pair."""
+    L = 8192
+    per_pair = 2 * 5 * L * 13 + 6 * L
+    return (ncols / 2) * per_pair
+
+
 def algorithmic_bytes(cfg: int, ncols: int, n: int | None = None) -> int:
     """Bytes of the minimal number of HBM passes per direction."""
     if cfg == 1:

@@ -556,8 +556,10 @@ inline int tma_variant() {
   if (v < 0) {
     // 1 (default): radix-32 stages, 3-deep landing ring for complex64 >= 1024
     // points; 3: radix-16 stages there too.  (Measured and dropped, round 1:
-    // single-buffer two-CTA-per-SM rings, 1/2/4-column complex128 tiles and
-    // radix-8 stages for 256..1024 points — all slower.)
+    // single-buffer two-CTA-per-SM rings, 1/2/4-column complex128 tiles,
+    // radix-8 stages for 256..1024 points, and radix-8 stages (16 warps per
+    // SM) for the complex128 512..2048-point passes of C5 (spectrum pass
+    // 2.72 -> 6.63 ms) — all slower.)
     const char* e = getenv("SMAT_TMA_VARIANT");
     v = e ? atoi(e) : 1;
   }

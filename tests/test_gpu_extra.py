@@ -164,3 +164,21 @@ def test_solvers_on_device_tensors(P):
     assert rel_l2(r.solution.cpu().numpy(), ref) < 1e-9
     t = sm.soft_threshold(rhs, 0.3)
     assert t.is_cuda and rel_l2(t.cpu().numpy(), orc.soft_threshold(P["cg_rhs"], 0.3)) < 1e-15
+
+
+def test_power_iteration_forked_plan_graph():
+    """A Sum with a LowRank term forks a side stream inside smat_apply; the
+    solver loop captures that fork/join into its CUDA graph."""
+    from paper_1710_09578_b200 import solvers
+
+    rng = np.random.default_rng(11)
+    N = 300
+    U = (rng.standard_normal((N, 4)) + 1j * rng.standard_normal((N, 4))) / np.sqrt(N)
+    V = (rng.standard_normal((N, 4)) + 1j * rng.standard_normal((N, 4))) / np.sqrt(N)
+    idx = np.arange(N)
+    op = sm.Sum(sm.Partial(sm.Hadamard(9), idx, idx), sm.LowRank(U, V))
+    oo = orc.sum_(orc.hadamard_padded(N), orc.lowrank(U, V))
+    got = sm.power_iteration(op, mode="singular", tol=1e-10, max_iter=300, seed=5)
+    assert solvers.last_loop_mode == "graph"
+    ref = orc.power_iteration(oo, mode="singular", tol=1e-10, max_iter=300, seed=5)
+    assert abs(got.value - ref[0]) < 1e-8 * ref[0] and got.converged == ref[3]
