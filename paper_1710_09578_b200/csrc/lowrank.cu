@@ -24,6 +24,14 @@ template <class P> struct LRT;
 template <> struct LRT<float2> { using R = float; };
 template <> struct LRT<double2> { using R = double; };
 
+// physical row of logical row r (LowRankArgs::rm_n1); chunks start on
+// multiples of 32 rows, so rows r0..r0+31 of a chunk stay contiguous
+__device__ __forceinline__ int64_t lr_phys(const LowRankArgs& a, int64_t r) {
+  if (a.rm_n1 == 0) return r;
+  const int64_t n1 = r % a.rm_n1, k2 = r / a.rm_n1;
+  return ((n1 >> 6) * a.rm_n2b + k2) * 64 + (n1 & 63);
+}
+
 template <class P> __device__ __forceinline__ P lr_zero() {
   using R = typename LRT<P>::R;
   return mk(R(0), R(0));
@@ -76,13 +84,14 @@ __global__ void __launch_bounds__(256, 2) lr_contract_kernel(const LowRankArgs a
   const int nch = r1 > r0 ? int((r1 - r0 + LR_RC - 1) / LR_RC) : 0;
   auto issue = [&](int ch) {
     const int64_t rr = r0 + int64_t(ch) * LR_RC;
+    const int64_t prr = lr_phys(a, rr);  // (a chunk is contiguous in either layout)
     P* xd = xs + (ch & 1) * LR_RC * LR_CT;
     P* fd = fs + (ch & 1) * LR_RC * 32;
     for (int l = tid; l < LR_RC * LR_CT; l += 256) {
       const int k = l / LR_CT, c = l % LR_CT;
       const int64_t row = rr + k, col = c0 + c;
       const bool ok = row < r1 && col < a.K;
-      cp_async<sizeof(P)>(&xd[l], ok ? &X[row * a.ldx + col] : X, ok);
+      cp_async<sizeof(P)>(&xd[l], ok ? &X[(prr + k) * a.ldx + col] : X, ok);
     }
     for (int l = tid; l < LR_RC * 32; l += 256) {
       const int k = l / 32, q = l % 32;
@@ -178,6 +187,7 @@ __global__ void __launch_bounds__(256, 1) lr_expand_kernel(const LowRankArgs a, 
   }
   for (int it = 0; ch < nchunks; ch += gridDim.x, ++it) {
     const int64_t r0 = ch * LR_RE;
+    const int64_t pr0 = lr_phys(a, r0);  // (a 32-row chunk is contiguous in either layout)
     // previous accumulate values of this chunk's outputs: in flight during the multiply
     P yv[4][4];
     if (a.accumulate) {
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(256, 1) lr_expand_kernel(const LowRankArgs a, 
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int64_t col = c0 + tx + 32 * j;
-          yv[i][j] = (row < a.rows && col < a.K) ? Y[row * a.ldy + col] : lr_zero<P>();
+          yv[i][j] = (row < a.rows && col < a.K) ? Y[(pr0 + ty + 8 * i) * a.ldy + col] : lr_zero<P>();
         }
       }
     }
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(256, 1) lr_expand_kernel(const LowRankArgs a, 
       for (int j = 0; j < 4; ++j) {
         const int64_t col = c0 + tx + 32 * j;
         if (col >= a.K) continue;
-        Y[row * a.ldy + col] = a.accumulate ? yv[i][j] + acc[i][j] : acc[i][j];
+        Y[(pr0 + ty + 8 * i) * a.ldy + col] = a.accumulate ? yv[i][j] + acc[i][j] : acc[i][j];
       }
     }
     __syncthreads();  // buffer (it & 1) is refilled two chunks later
@@ -537,13 +547,13 @@ static int expand_dmma_go(const LowRankArgs& a, int device, cudaStream_t s, bool
 }
 
 int launch_lowrank_contract(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry) {
-  if (dt == SMAT_C128 && lr_dmma()) return contract_dmma_go(a, device, s, dry);
+  if (dt == SMAT_C128 && lr_dmma() && !a.rm_n1) return contract_dmma_go(a, device, s, dry);
   if (dt == SMAT_C128) return contract_go<double2>(a, device, s, dry);
   if (dt == SMAT_C64) return contract_go<float2>(a, device, s, dry);
   throw Error(SMAT_UNSUPPORTED, "lowrank kernels: complex plans only");
 }
 int launch_lowrank_expand(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry) {
-  if (dt == SMAT_C128 && lr_dmma()) return expand_dmma_go(a, device, s, dry);
+  if (dt == SMAT_C128 && lr_dmma() && !a.rm_n1) return expand_dmma_go(a, device, s, dry);
   if (dt == SMAT_C128) return expand_go<double2>(a, device, s, dry);
   if (dt == SMAT_C64) return expand_go<float2>(a, device, s, dry);
   throw Error(SMAT_UNSUPPORTED, "lowrank kernels: complex plans only");

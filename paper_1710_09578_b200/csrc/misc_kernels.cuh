@@ -91,6 +91,10 @@ struct LowRankArgs {
   const void* s = nullptr;  // r or null
   int32_t s_conj = 0, accumulate = 0;
   int64_t rows = 0, r = 0, K = 0, ldx = 0, ldy = 0;
+  // blocked four-step row layout of the block side (x for contract, y for
+  // expand) when rm_n1 > 0: logical row r = n1 + rm_n1*k2 is stored at row
+  // ((n1 / 64) * rm_n2b + k2) * 64 + n1 % 64 (rm_n1 a multiple of 64)
+  int64_t rm_n1 = 0, rm_n2b = 0;
 };
 // number of launches (dry) or launch
 int launch_lowrank_contract(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry);

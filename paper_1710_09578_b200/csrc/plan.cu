@@ -332,6 +332,12 @@ struct XformIO {
   const void* post_fs = nullptr;
   bool conj_x = false, conj_y = false, inv = false, acc = false;
   double scale = 1.0;
+  // x (pass 1) / y (pass 3) already in the blocked four-step row layout of
+  // this transform: logical row n1 + N1*k2 at ((n1 / 64) * blk_n2b + k2) * 64 +
+  // n1 % 64 (rows of `inner` elements) — the DFSumNode chain keeps its
+  // intermediate there, so neither outer pass walks 2 MB-page strides
+  bool x_blk = false, y_blk = false;
+  int64_t blk_n2b = 0;
 };
 
 static void xform_pass_common(FftArgs& a, Ctx& c) {
@@ -361,6 +367,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   const int cdt = cplx_of(c.dt);
   const bool dbl = cdt == SMAT_C128;
   if (!fourstep(Nt, io.mid != nullptr, cdt)) {
+    SMAT_CHECK(!io.x_blk && !io.y_blk, SMAT_UNSUPPORTED, "blocked rows need a four-step transform");
     FftArgs a;
     fill_views(a, io.x, io.y, g);
     xform_pass_common(a, c);
@@ -409,6 +416,8 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   // row in its own 2 MB page (translation-bound, tools/tma_probe.cu).  Only
   // the user-layout side of the outer passes stays strided.
   const bool blk = O == 1 && N1 >= 128 && blocked_w();
+  SMAT_CHECK(blk || (!io.x_blk && !io.y_blk), SMAT_UNSUPPORTED, "blocked rows need the blocked four-step path");
+  SMAT_CHECK(!io.y_blk || io.mid, SMAT_UNSUPPORTED, "blocked output rows need the convolution passes");
   constexpr int BL = 6;
   const int64_t B = int64_t(1) << BL;
   // ---- pass 1: x -> W
@@ -419,6 +428,9 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.xs1 = B * io.x.si; a.xs2 = io.x.si; a.xsi = N1 * io.x.si;  // (n1 / B, n1 % B, k2)
     a.y = W.p; a.y_real = 0;
     a.ys1 = N2 * B * ic; a.ys2 = ic; a.ysi = B * ic;
+    if (io.x_blk) {  // x in the blocked row layout too
+      a.xs1 = io.blk_n2b * B * ic; a.xs2 = ic; a.xsi = B * ic;
+    }
     a.n2 = B; a.inner = ic; a.nb = N1 * ic;
     a.g_div = ic; a.g_mod = N1; a.gin_stride = N1;
     a.n_valid_in = io.x_rows;
@@ -506,6 +518,9 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       if (blk) {  // (n1 / B, n1 % B, k2) as in pass 1
         a.xs1 = N2 * B * ic; a.xs2 = ic; a.xsi = B * ic;
         a.ys1 = B * io.y.si; a.ys2 = io.y.si; a.ysi = N1 * io.y.si;
+        if (io.y_blk) {
+          a.ys1 = io.blk_n2b * B * ic; a.ys2 = ic; a.ysi = B * ic;
+        }
         a.n2 = B; a.inner = ic; a.nb = N1 * ic;
       }
       a.g_div = ic; a.g_mod = N1; a.gout_stride = N1;
@@ -676,18 +691,23 @@ struct LowRankNode : Node {
   }
   size_t w_bytes(const Ctx& c, const Geo& g) const { return size_t(r) * size_t(g.inner) * dt_size(c.dt); }
   // W = F^H x (row-slab reduction)
-  void contract(Ctx& c, bool adj, const Blk& x, const Geo& g, void* w) const {
+  // (rm_n1 / rm_n2b: x rows in a blocked four-step layout, LowRankArgs)
+  void contract(Ctx& c, bool adj, const Blk& x, const Geo& g, void* w, int64_t rm_n1 = 0,
+                int64_t rm_n2b = 0) const {
     LowRankArgs la;
     la.F = (adj ? U : V)->p; la.x = x.p; la.w = w; la.rows = adj ? rows : cols; la.r = r;
     la.K = g.inner; la.ldx = x.si;
+    la.rm_n1 = rm_n1; la.rm_n2b = rm_n2b;
     c.lr_contract(la);
   }
   // y (+)= G diag(s) W
-  void expand(Ctx& c, bool adj, const void* w, const Blk& y, const Geo& g, bool acc) const {
+  void expand(Ctx& c, bool adj, const void* w, const Blk& y, const Geo& g, bool acc, int64_t rm_n1 = 0,
+              int64_t rm_n2b = 0) const {
     LowRankArgs lb;
     lb.F = (adj ? V : U)->p; lb.w = const_cast<void*>(w); lb.y = y.p; lb.rows = adj ? cols : rows; lb.r = r;
     lb.K = g.inner; lb.ldy = y.si;
     lb.s = s ? s->p : nullptr; lb.s_conj = adj; lb.accumulate = acc;
+    lb.rm_n1 = rm_n1; lb.rm_n2b = rm_n2b;
     c.lr_expand(lb);
   }
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
@@ -970,6 +990,126 @@ struct SumNode : Node {
     for (size_t i = 0; i < t.size(); ++i) {
       const Blk& xi = t[i]->accepts_real() ? x0 : xc;
       t[i]->apply(c, adj, xi, y, g, acc || i > 0);
+    }
+    c.release(m0);
+  }
+};
+
+// Diag·Fourier·Diag (Bluestein, four-step) · Sum(PaddedHadamard, LowRank) —
+// the BASELINE C5 chain — with the Sum's result (forward) / operand (backward)
+// kept in the blocked four-step row layout of the Bluestein transform
+// (XformIO::x_blk / y_blk): logical row r = n1 + N1*k2 (N1 = the middle-pass
+// length) lives at row ((n1 / 64) * N2b + k2) * 64 + n1 % 64 of a P-row block
+// (P = 2^order, N2b = P / N1).  The padded Hadamard H_P = H_{N2b} (x) H_{N1}
+// splits along the same index: pass A transforms n1 (N1 contiguous user rows,
+// written blocked), pass B transforms k2 (64-row-strided blocked rows on both
+// sides), so every HBM pass of the chain except the user-layout side of the
+// FFT's far pass walks contiguous 64-row blocks instead of 2-4 MB row strides
+// (each row in its own 2 MB page: translation-bound).  The
+// rank-r contraction runs on the side stream against the user-layout block;
+// the expansion addresses the blocked rows through LowRankArgs::rm_n1.
+struct DFSumNode : Node {
+  Node* fallback = nullptr;       // the generic Product (used when a view does not qualify)
+  DiagFourierNode* df = nullptr;
+  Node* hp = nullptr;             // PaddedHadamard term
+  LowRankNode* lr = nullptr;
+  int64_t N1 = 0, N2 = 0, N2b = 0, P = 0, M = 0;
+  std::string describe() const override { return "BlockedChain(" + fallback->describe() + ")"; }
+  bool accepts_real() const override { return false; }
+  bool usable(const Ctx& c, const Blk& x, const Blk& y, const Geo& g, bool acc) const {
+    return !acc && c.dt == SMAT_C128 && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner &&
+           blocked_w() && lr->split_ok(c, x, y, g);
+  }
+  static WhtArgs wht_args(const void* x, void* y) {
+    WhtArgs a;
+    a.x = x; a.y = y;
+    return a;
+  }
+  // pass A: 2^a-point transform over n1 (user rows r = n1 + N1*k2 <-> blocked)
+  void pass_a(Ctx& c, const void* x, void* y, bool to_blocked, int64_t K, int64_t n) const {
+    WhtArgs a = wht_args(x, y);
+    a.n2 = N2b; a.inner = K; a.nb = N2b * K;
+    const int64_t blk_lo = K, blk_hi = N2b * 64 * K;
+    // (the row split applies to both sides: the natural side's high stride is 64 rows)
+    if (to_blocked) {  // natural in, blocked out (forward)
+      a.xs2 = N1 * K; a.xsi = K; a.xsi_hi = 64 * K;
+      a.ys2 = 64 * K; a.ysi = blk_lo; a.ysi_hi = blk_hi;
+      a.n_valid_in = n;   // rows >= n are the zero padding
+    } else {           // blocked in, natural out (backward)
+      a.xs2 = 64 * K; a.xsi = blk_lo; a.xsi_hi = blk_hi;
+      a.ys2 = N1 * K; a.ysi = K; a.ysi_hi = 64 * K;
+      a.n_valid_out = n;  // rows >= n are truncated
+    }
+    a.i_lo_bits = 6;
+    a.g_div = K; a.g_mod = N2b; a.g_mul = N1; a.gin_stride = 1; a.gout_stride = 1;
+    c.wht(c.dt, int(N1), a);
+  }
+  // pass B: N2b-point transform over k2, blocked on both sides
+  void pass_b(Ctx& c, const void* x, void* y, bool mask_in, int64_t K, int64_t n) const {
+    WhtArgs a = wht_args(x, y);
+    a.xs1 = a.ys1 = N2b * 64 * K; a.xs2 = a.ys2 = K; a.xsi = a.ysi = 64 * K;
+    a.n2 = 64; a.inner = K; a.nb = N1 * K;
+    a.g_div = K; a.g_mod = N1; a.g_mul = 1; a.gin_stride = a.gout_stride = N1;
+    if (mask_in) a.n_valid_in = n;   // backward: unwritten rows >= n read as zero
+    else a.n_valid_out = n;          // forward: rows >= n are not stored
+    c.wht(c.dt, int(N2b), a);
+  }
+  XformIO df_io(bool adj, const Blk& x, const Blk& y, int64_t n) const {
+    XformIO io;
+    io.x = x; io.x_rows = n; io.y = y; io.y_rows = n;
+    io.pre = (adj ? df->vl : df->vr) ? (adj ? df->vl : df->vr)->p : nullptr;
+    io.post = (adj ? df->vr : df->vl) ? (adj ? df->vr : df->vl)->p : nullptr;
+    io.pre_fs = (adj ? df->vl_fs : df->vr_fs) ? (adj ? df->vl_fs : df->vr_fs)->p : nullptr;
+    io.post_fs = (adj ? df->vr_fs : df->vl_fs) ? (adj ? df->vr_fs : df->vl_fs)->p : nullptr;
+    io.conj_x = adj; io.conj_y = adj;
+    io.mid = df->F->kspec->p;
+    io.scale = 1.0 / double(M);
+    io.blk_n2b = N2b;
+    return io;
+  }
+  void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
+    const size_t m0 = c.mark();
+    Blk x = promote(c, x0, g, adj ? rows : cols);
+    if (!usable(c, x, y, g, acc)) {
+      fallback->apply(c, adj, x, y, g, acc);
+      c.release(m0);
+      return;
+    }
+    const int64_t K = g.inner, n = rows;
+    Geo gb;
+    gb.inner = K;
+    Blk Tb = c.alloc_blk(c.dt, gb, P);   // blocked
+    Blk Tmp = c.alloc_blk(c.dt, gb, P);  // blocked
+    void* w = c.alloc(lr->w_bytes(c, g));
+    const bool fork = c.can_fork();
+    if (!adj) {
+      // y = DF (H_pad x + U diag(s) V^H x)
+      Ctx side = c;
+      if (fork) side.stream = c.fork();
+      side.launches = 0;
+      lr->contract(side, false, x, g, w);
+      c.launches += side.launches;
+      pass_a(c, x.p, Tmp.p, true, K, n);
+      pass_b(c, Tmp.p, Tb.p, false, K, n);
+      if (fork) c.join(side.stream);
+      lr->expand(c, false, w, Tb, g, true, N1, N2b);
+      XformIO io = df_io(false, Tb, y, n);
+      io.x_blk = true;
+      run_xform(c, M, g, io);
+    } else {
+      // y = (H_pad + V diag(conj s) U^H) DF^H x
+      XformIO io = df_io(true, x, Tb, n);
+      io.y_blk = true;
+      run_xform(c, M, g, io);
+      Ctx side = c;
+      if (fork) side.stream = c.fork();
+      side.launches = 0;
+      lr->contract(side, true, Tb, g, w, N1, N2b);
+      c.launches += side.launches;
+      pass_b(c, Tb.p, Tmp.p, true, K, n);
+      pass_a(c, Tmp.p, y.p, false, K, n);
+      if (fork) c.join(side.stream);
+      lr->expand(c, true, w, y, g, true);
     }
     c.release(m0);
   }
@@ -1375,6 +1515,37 @@ struct Builder {
     }
   }
 
+  // [DiagFourier (Bluestein, four-step), Sum(PaddedHadamard, LowRank)] ->
+  // DFSumNode (the BASELINE C5 chain), when the Hadamard length factors over
+  // the Bluestein transform's middle-pass length
+  Node* blocked_chain(ProductNode* prod) {
+    if (p.dt != SMAT_C128) return nullptr;
+    auto* df = dynamic_cast<DiagFourierNode*>(prod->f[0]);
+    auto* sum = dynamic_cast<SumNode*>(prod->f[1]);
+    if (!df || !sum || !df->F->M || sum->t.size() != 2) return nullptr;
+    PartialNode* hp = nullptr;
+    LowRankNode* lr = nullptr;
+    for (Node* t : sum->t) {
+      if (auto* q = dynamic_cast<PartialNode*>(t); q && q->had_order >= 0) hp = q;
+      if (auto* q = dynamic_cast<LowRankNode*>(t)) lr = q;
+    }
+    if (!hp || !lr || lr->r > 32) return nullptr;
+    const int64_t M = df->F->M, n = df->F->n;
+    if (!fourstep(M, true, SMAT_C128)) return nullptr;
+    int64_t N1, N2;
+    fourstep_split(M, N1, N2);
+    const int64_t P = int64_t(1) << hp->had_order;
+    if (N1 < 128 || N1 > kTileMax || P % N1 || P < n || hp->rows != n || hp->cols != n) return nullptr;
+    const int64_t N2b = P / N1;
+    if (N2b < 2 || N2b > N2 || N2b > kTileMax) return nullptr;
+    auto* b = add<DFSumNode>();
+    b->fallback = prod;
+    b->df = df; b->hp = hp; b->lr = lr;
+    b->N1 = N1; b->N2 = N2; b->N2b = N2b; b->P = P; b->M = M;
+    p.fused = "blocked Bluestein/Hadamard/LowRank chain (N1=" + std::to_string(N1) + ", N2b=" + std::to_string(N2b) + ")";
+    return b;
+  }
+
   std::vector<Node*> memo;  // shared sub-operators are compiled once
 
   Node* build(int idx) {
@@ -1526,6 +1697,9 @@ struct Builder {
           SMAT_CHECK(a->f[k]->cols == a->f[k + 1]->rows, SMAT_BAD_SHAPE, "product chain mismatch");
         fuse_diag_fourier(a->f);
         out = a->f.size() == 1 ? a->f[0] : a;
+        if (a->f.size() == 2) {
+          if (Node* bc = blocked_chain(a)) out = bc;
+        }
         break;
       }
       case SMAT_SUM: {

@@ -104,6 +104,9 @@ struct WhtDev {
   // masks (MASK instantiation only)
   FastDiv gdiv, gmod;
   int32_t g_mul, gin_stride, gout_stride, n_valid_in, n_valid_out;
+  // two-level rows: (i & i_lo_mask) * si + (i >> i_lo_bits) * si_hi
+  int32_t i_lo_bits, i_lo_mask;
+  int64_t xsi_hi, ysi_hi;
 };
 
 // b -> (o1, o2, c) with b = (o1*n2 + o2)*inner + c; returns the offset of the
@@ -341,7 +344,8 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
       const int i = bb * R0 + r;
       bool ok = act;
       if constexpr (MASK) ok = ok && goff + i * p.gin_stride < p.n_valid_in;
-      a[u * R0 + r] = ok ? x[int64_t(i) * p.xsi] : zero_of<T>();
+      a[u * R0 + r] =
+          ok ? x[int64_t(i & p.i_lo_mask) * p.xsi + int64_t(i >> p.i_lo_bits) * p.xsi_hi] : zero_of<T>();
     }
   }
   wht_stages<T, N, E, CT, 0>(a, sm, j, cs);
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
       if constexpr (MASK) {
         if (goff + k * p.gout_stride >= p.n_valid_out) continue;
       }
-      const int64_t off = int64_t(k) * p.ysi;
+      const int64_t off = int64_t(k & p.i_lo_mask) * p.ysi + int64_t(k >> p.i_lo_bits) * p.ysi_hi;
       y[off] = p.acc ? y[off] + a[u * RL + r] : a[u * RL + r];
     }
   }
@@ -493,6 +497,10 @@ inline void wht_tile_launch(const WhtArgs& a, cudaStream_t s) {
   d.n2 = FastDiv(a.n2);
   d.nb = int32_t(a.nb);
   d.acc = a.accumulate;
+  d.i_lo_bits = a.i_lo_bits;
+  d.i_lo_mask = a.i_lo_bits ? (1 << a.i_lo_bits) - 1 : -1;
+  d.xsi_hi = a.i_lo_bits ? a.xsi_hi : 0;
+  d.ysi_hi = a.i_lo_bits ? a.ysi_hi : 0;
   const int64_t gmax_in = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gin_stride;
   const int64_t gmax_out = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gout_stride;
   const bool mask = gmax_in >= a.n_valid_in || gmax_out >= a.n_valid_out;

@@ -68,6 +68,10 @@ struct WhtArgs {
   int64_t g_div = 1, g_mod = 1, g_mul = 1, gin_stride = 1, gout_stride = 1;
   int64_t n_valid_in = INT64_MAX, n_valid_out = INT64_MAX;
   int32_t accumulate = 0;
+  // two-level rows (blocked layouts): row i at (i % 2^i_lo_bits) * {x,y}si +
+  // (i >> i_lo_bits) * {x,y}si_hi when i_lo_bits > 0
+  int32_t i_lo_bits = 0;
+  int64_t xsi_hi = 0, ysi_hi = 0;
 };
 
 constexpr int kTileMax = 4096;

@@ -365,3 +365,24 @@ def test_to_dense_and_blocks():
     _close(op.to_dense(), ref, 1e-13, "blocks dense")
     _close(sm.Hadamard(1).to_dense(), [[1, 1], [1, -1]], 0, "H1")
     _close(sm.Fourier(2).to_dense(), [[1, 1], [1, -1]], 1e-15, "F2")
+
+
+@pytest.mark.parametrize("N,K", [(5003, 4), (5003, 3), (70001, 8), (70001, 64)])
+def test_c5_blocked_chain(N, K):
+    """The C5 chain at four-step sizes compiles into the blocked chain
+    (DFSumNode: blocked Sum intermediate, split Hadamard, row-mapped LowRank)
+    and matches the oracle forward and backward to 1e-12."""
+    rng = np.random.default_rng(N + K)
+    d1 = np.exp(2j * np.pi * rng.random(N))
+    d2 = np.exp(2j * np.pi * rng.random(N))
+    U = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    V = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    idx = np.arange(N)
+    order = (N - 1).bit_length()
+    op = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2),
+                    sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx), sm.LowRank(U, V)))
+    assert "BlockedChain" in op.plan_for(np.complex128).describe()
+    oo = orc.chain_c5(N, d1, d2, U, V)
+    X = (rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))) / np.sqrt(2)
+    _close(op.forward(X), orc.apply(oo, X, 0), 1e-12, f"C5 blocked fwd N={N} K={K}")
+    _close(op.backward(X), orc.apply(oo, X, 1), 1e-12, f"C5 blocked bwd N={N} K={K}")
