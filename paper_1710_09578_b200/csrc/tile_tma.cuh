@@ -566,8 +566,26 @@ inline int tma_variant() {
   return v;
 }
 
+// complex128 1024-point passes: one landing buffer per CTA and two CTAs (16
+// warps) per SM (default; SMAT_TMA_C128_NB1=0 -> two landing buffers, one CTA).
+// These passes are issue-latency bound at 8 warps per SM (ncu: 26% issue
+// utilisation, 0.4 eligible warps per scheduler); the second CTA hides more
+// of it than the lost load lead costs (C5 outer passes 2.34 / 2.00 ->
+// 2.09 / 1.78 ms), despite ~300 B of register spills at 128 registers.
+inline bool tma_c128_nb1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMAT_TMA_C128_NB1");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
+  if constexpr (N == 1024 && sizeof(C) == 16) {
+    if (tma_c128_nb1()) return fft_tma_launch_v<C, N, 16, 1>(a, s);
+  }
   if constexpr (N >= 1024 && sizeof(C) == 8) {
     if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
   }
