@@ -556,7 +556,10 @@ inline int tma_variant() {
   if (v < 0) {
     // 1 (default): radix-32 stages, 3-deep landing ring for complex64 >= 1024
     // points; 3: radix-16 stages there too.  (Measured and dropped, round 1:
-    // single-buffer two-CTA-per-SM rings, 1/2/4-column complex128 tiles,
+    // single-buffer two-CTA-per-SM rings (except complex128 1024, above),
+    // the complex128 2048-point spectrum pass with one landing buffer and its
+    // spectrum slice read from L2 so two CTAs fit (2.73 -> 3.49 ms),
+    // 1/2/4-column complex128 tiles,
     // radix-8 stages for 256..1024 points, and radix-8 stages (16 warps per
     // SM) for the complex128 512..2048-point passes of C5 (spectrum pass
     // 2.72 -> 6.63 ms) — all slower.)
