@@ -16,6 +16,12 @@ for w in c1 c2 c3 c4 c5; do
   python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
   echo "bench $w rc=$?"
 done
+python bench.py --workload cg --steps 20 --warmup 4 > gpurun_out/bench_cg.json 2> gpurun_out/bench_cg.err
+echo "bench cg rc=$?"
+python tools/prof_cg.py 4 > gpurun_out/plain_cg.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_cg.csv python tools/prof_cg.py 4 > gpurun_out/ncu_cg.log 2>&1
+echo "launches cg rc=$?"
 for w in 2 1 3 4 5; do
   python tools/prof_c2.py $w 1 > gpurun_out/plain_c$w.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
@@ -26,3 +32,9 @@ python tools/prof_c2.py 2 1 > /dev/null 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:fft_tma_kernel -c 3 \
       -o gpurun_out/full_c2 python tools/prof_c2.py 2 1 > gpurun_out/ncu_full_c2.log 2>&1
 echo "full c2 rc=$?"
+python tools/prof_c2.py 5 1 > /dev/null 2>&1 && \
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"fft_tma|wht_tile|lr_" -c 9 \
+      -o gpurun_out/full_c5 python tools/prof_c2.py 5 1 > gpurun_out/ncu_full_c5.log 2>&1
+echo "full c5 rc=$?"
+python tools/ncu_summary.py gpurun_out/full_c2.ncu-rep > gpurun_out/full_c2_summary.txt 2>&1
+python tools/ncu_summary.py gpurun_out/full_c5.ncu-rep > gpurun_out/full_c5_summary.txt 2>&1
