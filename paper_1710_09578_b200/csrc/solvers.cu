@@ -119,13 +119,32 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(int64_t n, int64_t K, i
   }
 }
 
+// Column totals of the partials, deterministic: one 128-thread block per
+// column, thread t sums row blocks t, t+128, ... in order, then a fixed-shape
+// shared-memory tree.  The finalising kernels run one block per column and
+// use the result in thread 0.
 template <int Q>
-__device__ __forceinline__ void col_sum(const double* part, int64_t K, int nb, int64_t c, double* out) {
+__device__ __forceinline__ bool col_sum(const double* part, int64_t K, int nb, int64_t c, double* out) {
+  __shared__ double red[128 * Q];
+  const int t = threadIdx.x;
+  double v[Q];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) out[q] = 0.0;
-  for (int b = 0; b < nb; ++b)
+  for (int q = 0; q < Q; ++q) v[q] = 0.0;
+  for (int b = t; b < nb; b += 128)
 #pragma unroll
-    for (int q = 0; q < Q; ++q) out[q] += part[(int64_t(b) * K + c) * Q + q];
+    for (int q = 0; q < Q; ++q) v[q] += part[(int64_t(b) * K + c) * Q + q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) red[t * Q + q] = v[q];
+  __syncthreads();
+  for (int h = 64; h > 0; h >>= 1) {
+    if (t < h)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) red[t * Q + q] += red[(t + h) * Q + q];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) out[q] = red[q];
+  return t == 0;
 }
 
 template <int Q, class F>
@@ -154,10 +173,9 @@ __global__ void cg_init_vec(const C* b, C* x, C* r, C* p, int64_t tot) {
   }
 }
 __global__ void cg_init_fin(const double* part, int nb, int64_t K, double tol, double* st) {
-  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= K) return;
+  const int64_t c = blockIdx.x;
   double rr;
-  col_sum<1>(part, K, nb, c, &rr);
+  if (!col_sum<1>(part, K, nb, c, &rr)) return;
   double* s = st + c * CG_NS;
   const double nr0 = sqrt(rr);
   s[CG_RS] = rr;
@@ -170,12 +188,11 @@ __global__ void cg_init_fin(const double* part, int nb, int64_t K, double tol, d
   s[CG_RES] = 0.0;
 }
 __global__ void cg_alpha_fin(const double* part, int nb, int64_t K, double* st) {
-  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= K) return;
+  const int64_t c = blockIdx.x;
   double* s = st + c * CG_NS;
-  if (s[CG_STATUS] != 0.0) return;
+  if (s[CG_STATUS] != 0.0) return;  // (uniform over the block)
   double v[3];
-  col_sum<3>(part, K, nb, c, v);
+  if (!col_sum<3>(part, K, nb, c, v)) return;
   const double curv = v[0], slack = 1e-14 * sqrt(v[1]) * sqrt(v[2]);
   if (curv <= slack) {  // BreakdownError (solvers.py:88-93)
     s[CG_STATUS] = 2.0;
@@ -186,12 +203,11 @@ __global__ void cg_alpha_fin(const double* part, int nb, int64_t K, double* st) 
   s[CG_ALPHA] = s[CG_RS] / curv;
 }
 __global__ void cg_beta_fin(const double* part, int nb, int64_t K, double max_iter, double* st) {
-  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= K) return;
+  const int64_t c = blockIdx.x;
   double* s = st + c * CG_NS;
-  if (s[CG_STATUS] != 0.0) return;
+  if (s[CG_STATUS] != 0.0) return;  // (uniform over the block)
   double rs_new;
-  col_sum<1>(part, K, nb, c, &rs_new);
+  if (!col_sum<1>(part, K, nb, c, &rs_new)) return;
   const double it = s[CG_ITERS] + 1.0;
   s[CG_ITERS] = it;
   if (sqrt(rs_new) <= s[CG_THR]) {  // converged (solvers.py:97-98)
@@ -220,7 +236,7 @@ void cg_init_t(int64_t n, int64_t K, const void* b, void* x, void* r, void* p, d
   const C* bb = (const C*)b;
   reduce<1>(n, K, [=] __device__(int64_t i, int64_t c, double* a) { a[0] += abs2_(bb[i * K + c]); }, part, s);
   cg_init_vec<C><<<blocks_for(n * K), 256, 0, s>>>(bb, (C*)x, (C*)r, (C*)p, n * K);
-  cg_init_fin<<<unsigned((K + 127) / 128), 128, 0, s>>>(part, int(rgeo(n, K).grid.y), K, tol, st);
+  cg_init_fin<<<unsigned(K), 128, 0, s>>>(part, int(rgeo(n, K).grid.y), K, tol, st);
   SMAT_CUDA(cudaGetLastError());
 }
 
@@ -232,7 +248,7 @@ void cg_step_t(int64_t n, int64_t K, void* x_, void* r_, void* p_, const void* a
   C* p = (C*)p_;
   const C* ap = (const C*)ap_;
   const int nb = int(rgeo(n, K).grid.y);
-  const unsigned cb = unsigned((K + 127) / 128);
+  const unsigned cb = unsigned(K);  // one finalising block per column
   // curvature Re<p, Ap>, |p|^2, |Ap|^2 (solvers.py:86-87)
   reduce<3>(
       n, K,
@@ -271,9 +287,8 @@ template <class C>
 void ista_residual_t(int64_t n, const void* b_, const void* mx_, void* r_, double* trace, double* st, double lam,
                      double* part, cudaStream_t s);
 __global__ void ista_trace_fin(const double* part, int nb, double lam, double* trace, double* st) {
-  if (threadIdx.x || blockIdx.x) return;
   double rr;
-  col_sum<1>(part, 1, nb, 0, &rr);
+  if (!col_sum<1>(part, 1, nb, 0, &rr)) return;
   const int64_t k = int64_t(st[1]);
   trace[k] = lam * st[0] + 0.5 * rr;  // solvers.py:185-187, 190-192
   st[1] = double(k + 1);
@@ -294,13 +309,12 @@ void ista_residual_t(int64_t n, const void* b_, const void* mx_, void* r_, doubl
         a[0] += abs2_(v);
       },
       part, s);
-  ista_trace_fin<<<1, 32, 0, s>>>(part, int(rgeo(n, 1).grid.y), lam, trace, st);
+  ista_trace_fin<<<1, 128, 0, s>>>(part, int(rgeo(n, 1).grid.y), lam, trace, st);
   SMAT_CUDA(cudaGetLastError());
 }
 __global__ void ista_l1_fin(const double* part, int nb, double* st) {
-  if (threadIdx.x || blockIdx.x) return;
   double l1;
-  col_sum<1>(part, 1, nb, 0, &l1);
+  if (!col_sum<1>(part, 1, nb, 0, &l1)) return;
   st[0] = l1;
 }
 template <class C>
@@ -317,7 +331,7 @@ void ista_update_t(int64_t n, void* x_, const void* g_, double alpha, double lev
         a[0] += abs_(v);
       },
       part, s);
-  ista_l1_fin<<<1, 32, 0, s>>>(part, int(rgeo(n, 1).grid.y), st);
+  ista_l1_fin<<<1, 128, 0, s>>>(part, int(rgeo(n, 1).grid.y), st);
   SMAT_CUDA(cudaGetLastError());
 }
 
@@ -325,11 +339,12 @@ void ista_update_t(int64_t n, void* x_, const void* g_, double alpha, double lev
 // state: [0] estimate, [1] iterations, [2] done, [3] converged, [4] 1/|w| of
 // this step (0: do not normalise), [5] zero flag
 __global__ void power_fin(const double* part, int nb, double tol, double* st) {
-  if (threadIdx.x || blockIdx.x) return;
-  st[4] = 0.0;
-  if (st[2] != 0.0) return;
+  const bool done = st[2] != 0.0;
+  __syncthreads();  // every thread has read `done` before thread 0 writes the state
   double v[3];
-  col_sum<3>(part, 1, nb, 0, v);
+  if (!col_sum<3>(part, 1, nb, 0, v)) return;
+  st[4] = 0.0;
+  if (done) return;
   const double it = st[1] + 1.0;
   st[1] = it;
   const double est_new = hypot(v[0], v[1]);  // |vdot(v, w)| (solvers.py:321-322)
@@ -369,7 +384,7 @@ void power_step_t(int64_t n, void* v_, const void* w_, double* st, double tol, d
         a[2] += abs2_(wv);
       },
       part, s);
-  power_fin<<<1, 32, 0, s>>>(part, int(rgeo(n, 1).grid.y), tol, st);
+  power_fin<<<1, 128, 0, s>>>(part, int(rgeo(n, 1).grid.y), tol, st);
   power_norm<C><<<blocks_for(n), 256, 0, s>>>(v, w, st, n);
   SMAT_CUDA(cudaGetLastError());
 }

@@ -575,19 +575,20 @@ inline int tma_variant() {
 // utilisation, 0.4 eligible warps per scheduler); the second CTA hides more
 // of it than the lost load lead costs (C5 outer passes 2.34 / 2.00 ->
 // 2.09 / 1.78 ms), despite ~300 B of register spills at 128 registers.
-inline bool tma_c128_nb1() {
+inline int tma_c128_nb1() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SMAT_TMA_C128_NB1");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = e ? atoi(e) : 1;
   }
-  return v == 1;
+  return v;
 }
 
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
   if constexpr (N == 1024 && sizeof(C) == 16) {
-    if (tma_c128_nb1()) return fft_tma_launch_v<C, N, 16, 1>(a, s);
+    // (spectrum passes keep two buffers: at 128 registers their FFT + IFFT spills)
+    if (tma_c128_nb1() == 2 || (tma_c128_nb1() == 1 && !a.mid)) return fft_tma_launch_v<C, N, 16, 1>(a, s);
   }
   if constexpr (N >= 1024 && sizeof(C) == 8) {
     if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
