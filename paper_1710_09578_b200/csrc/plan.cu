@@ -194,6 +194,27 @@ __global__ void vec_mul_kernel(const C* a, const C* b, C* o, int64_t n) {
     o[i] = cmul(a[i], b[i]);
 }
 
+// out[i][q] = a[i][q] * (conj?) s[q]   (rows x r, row-major)
+__global__ void scale_cols_kernel(const double2* a, const double2* sv, int conj_s, double2* out, int64_t rows,
+                                  int64_t r) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * r; e += int64_t(gridDim.x) * blockDim.x) {
+    double2 w = sv[e % r];
+    if (conj_s) w.y = -w.y;
+    out[e] = cmul(a[e], w);
+  }
+}
+// Blocked-row copy of a (n x r) row-major factor into P rows: logical row
+// t = n1 + N1*k2 at ((n1 / 64) * N2b + k2) * 64 + n1 % 64, zero for t >= n.
+__global__ void block_rows_kernel(const double2* a, double2* out, int64_t n, int64_t r, int64_t N1, int64_t N2b) {
+  const int64_t P = N1 * N2b;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < P * r; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = e / r, q = e % r;
+    const int64_t n1 = t % N1, k2 = t / N1;
+    const int64_t ph = ((n1 >> 6) * N2b + k2) * 64 + (n1 & 63);
+    out[ph * r + q] = t < n ? a[e] : make_double2(0.0, 0.0);
+  }
+}
+
 __global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const float c = float(a[i].x), s = float(a[i].y);
@@ -683,7 +704,15 @@ struct DenseNode : Node {
 struct LowRankNode : Node {
   DevBuf *U = nullptr, *V = nullptr, *s = nullptr;
   int64_t r = 0;
-  std::string describe() const override { return "LowRank(rank " + std::to_string(r) + ")"; }
+  // complex128 plans with cuBLAS: the expansion factors with the diagonal
+  // folded in (U diag(s), V diag(conj s); U / V themselves when s is absent)
+  // and, for the DFSumNode chain, blocked-row copies of U (P rows, zero past
+  // the operator's rows)
+  DevBuf *Us = nullptr, *Vs = nullptr, *Ub = nullptr, *Ubs = nullptr;
+  bool blas = false;
+  std::string describe() const override {
+    return "LowRank(rank " + std::to_string(r) + (blas ? ", cuBLAS ZGEMM" : "") + ")";
+  }
   // tall-skinny rank-r kernels apply (complex plan, single batch, row-contiguous)
   bool split_ok(const Ctx& c, const Blk& x, const Blk& y, const Geo& g) const {
     return dt_complex(c.dt) && x.dt == c.dt && r <= 32 && g.n1 * g.n2 == 1 && x.si == g.inner &&
@@ -694,6 +723,16 @@ struct LowRankNode : Node {
   // (rm_n1 / rm_n2b: x rows in a blocked four-step layout, LowRankArgs)
   void contract(Ctx& c, bool adj, const Blk& x, const Geo& g, void* w, int64_t rm_n1 = 0,
                 int64_t rm_n2b = 0) const {
+    if (blas) {
+      // W' (K x r, column-major) = X' (K x rows) F'^H, F' = (r x rows); blocked
+      // rows: all P rows of the blocked block against the blocked copy of U
+      const bool blk = rm_n1 > 0;
+      SMAT_CHECK(!blk || adj, SMAT_UNSUPPORTED, "blocked contraction is the adjoint's");
+      const int64_t n = blk ? Ub->len / r : (adj ? rows : cols);
+      const void* F = blk ? Ub->p : (adj ? U : V)->p;
+      c.zgemm(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner, true, "zgemm3m_contract");
+      return;
+    }
     LowRankArgs la;
     la.F = (adj ? U : V)->p; la.x = x.p; la.w = w; la.rows = adj ? rows : cols; la.r = r;
     la.K = g.inner; la.ldx = x.si;
@@ -703,6 +742,15 @@ struct LowRankNode : Node {
   // y (+)= G diag(s) W
   void expand(Ctx& c, bool adj, const void* w, const Blk& y, const Geo& g, bool acc, int64_t rm_n1 = 0,
               int64_t rm_n2b = 0) const {
+    if (blas) {
+      // Y' (K x rows) (+)= W' (K x r) G'  with G = U diag(s) / V diag(conj s)
+      const bool blk = rm_n1 > 0;
+      SMAT_CHECK(!blk || !adj, SMAT_UNSUPPORTED, "blocked expansion is the forward's");
+      const int64_t n = blk ? Ubs->len / r : (adj ? cols : rows);
+      const void* G = blk ? Ubs->p : (adj ? Vs : Us)->p;
+      c.zgemm(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si, false, "zgemm_expand");
+      return;
+    }
     LowRankArgs lb;
     lb.F = (adj ? V : U)->p; lb.w = const_cast<void*>(w); lb.y = y.p; lb.rows = adj ? cols : rows; lb.r = r;
     lb.K = g.inner; lb.ldy = y.si;
@@ -1100,6 +1148,7 @@ struct DFSumNode : Node {
       // y = (H_pad + V diag(conj s) U^H) DF^H x
       XformIO io = df_io(true, x, Tb, n);
       io.y_blk = true;
+      io.y_rows = P;  // rows n..P come out zero (zero-padded post vector): finite for the P-row contraction
       run_xform(c, M, g, io);
       Ctx side = c;
       if (fork) side.stream = c.fork();
@@ -1542,6 +1591,16 @@ struct Builder {
     b->fallback = prod;
     b->df = df; b->hp = hp; b->lr = lr;
     b->N1 = N1; b->N2 = N2; b->N2b = N2b; b->P = P; b->M = M;
+    if (lr->blas) {
+      lr->Ub = new_buf(p, SMAT_C128, P * lr->r);
+      block_rows_kernel<<<1184, 256>>>((const double2*)lr->U->p, (double2*)lr->Ub->p, n, lr->r, N1, N2b);
+      lr->Ubs = lr->Ub;
+      if (lr->s) {
+        lr->Ubs = new_buf(p, SMAT_C128, P * lr->r);
+        block_rows_kernel<<<1184, 256>>>((const double2*)lr->Us->p, (double2*)lr->Ubs->p, n, lr->r, N1, N2b);
+      }
+      SMAT_CUDA(cudaGetLastError());
+    }
     p.fused = "blocked Bluestein/Hadamard/LowRank chain (N1=" + std::to_string(N1) + ", N2b=" + std::to_string(N2b) + ")";
     return b;
   }
@@ -1580,6 +1639,21 @@ struct Builder {
         n->U = upload_param(p, nd.param[0], p.dt);
         n->V = upload_param(p, nd.param[1], p.dt);
         if (nd.param[2].len) n->s = upload_param(p, nd.param[2], p.dt);
+        if (p.dt == SMAT_C128 && blas_available() && n->r <= 32) {
+          n->blas = true;
+          blas_warm(p.device);
+          n->Us = n->U;
+          n->Vs = n->V;
+          if (n->s) {
+            n->Us = new_buf(p, SMAT_C128, n->U->len);
+            n->Vs = new_buf(p, SMAT_C128, n->V->len);
+            scale_cols_kernel<<<1184, 256>>>((const double2*)n->U->p, (const double2*)n->s->p, 0,
+                                             (double2*)n->Us->p, nd.rows, n->r);
+            scale_cols_kernel<<<1184, 256>>>((const double2*)n->V->p, (const double2*)n->s->p, 1,
+                                             (double2*)n->Vs->p, nd.cols, n->r);
+            SMAT_CUDA(cudaGetLastError());
+          }
+        }
         out = n;
         break;
       }
