@@ -156,3 +156,24 @@ def test_solver_validation_cpu():
     assert sm.Power(H, 4).footprint_bytes() == 16 + H.footprint_bytes()
     par = sm.Parametric(lambda i, j: i + j, 3, 4, sm.ScalarField.REAL64)
     assert par.shape == (3, 4) and par.footprint_bytes() == 24
+
+
+def test_selfcheck_dense_definitions():
+    """The self-verification zoo's dense matrices (selfcheck.py) agree with the
+    oracle's dense materialisations of the same operators."""
+    from paper_1710_09578_b200 import selfcheck as sc
+
+    rng = np.random.default_rng(3)
+    for order in range(0, 6):
+        assert np.array_equal(sc.hadamard_matrix(order), orc.to_dense(orc.hadamard(order)))
+    for n in (1, 2, 5, 8, 12):
+        assert np.allclose(sc.dft_matrix(n), orc.to_dense(orc.fourier(n)), atol=1e-12)
+        c = rng.standard_normal(n)
+        assert np.allclose(sc.circulant_matrix(c), orc.to_dense(orc.circulant(c)), atol=1e-12)
+    for n, m in ((1, 1), (3, 5), (6, 2), (7, 7)):
+        col, rest = rng.standard_normal(n), rng.standard_normal(m - 1)
+        assert np.allclose(sc.toeplitz_matrix(col, rest), orc.to_dense(orc.toeplitz(col, rest)), atol=1e-12)
+    names = {name for name, _, _ in sc.build_zoo(max_size=16)}
+    assert names == {"Dense", "Zero", "Identity", "Diagonal", "Sparse", "Fourier", "Circulant", "Toeplitz",
+                     "Parametric", "Hadamard", "Product", "Kron", "Blocks", "BlockDiag", "Partial", "Polynomial",
+                     "Power", "Adjoint"}

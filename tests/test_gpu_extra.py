@@ -182,3 +182,15 @@ def test_power_iteration_forked_plan_graph():
     assert solvers.last_loop_mode == "graph"
     ref = orc.power_iteration(oo, mode="singular", tol=1e-10, max_iter=300, seed=5)
     assert abs(got.value - ref[0]) < 1e-8 * ref[0] and got.converged == ref[3]
+
+
+def test_selfcheck_zoo_device():
+    """The reference's self-verification suite (verify.py) over every operator
+    class, on the device: all instances PASS."""
+    from paper_1710_09578_b200 import selfcheck
+
+    lines = []
+    res = selfcheck.run_verification(max_size=64, seed=0, emit=lines.append)
+    failed = [l for l in lines if l.startswith("FAIL")]
+    assert not failed, "\n".join(failed)
+    assert len(res) >= 50 and all(r.passed for r in res)
