@@ -33,12 +33,35 @@ from .errors import DimensionMismatch, MaterializationTooLarge
 
 DEFAULT_DENSE_CAP_BYTES = 2 ** 31  # 2 GiB materialization guard (core.py:16)
 
-# Host inputs whose (rows x K) block exceeds this many bytes are streamed
-# through the device in column chunks (H2D copies, device passes and D2H
-# copies of different chunks overlap on three streams); smaller blocks move as
-# one contiguous DMA each way, which is what saturates the host link — a
-# column chunk of a row-major block is a pitched copy of short rows.
-HOST_CHUNK_BYTES = 8 << 30
+# Host blocks of at least this many bytes are streamed through the device in
+# column chunks: H2D copies, device passes and D2H copies of different chunks
+# overlap on three streams.  A column chunk of a row-major block is a pitched
+# copy; the box copies 512- and 256-byte rows at the full link rate (~55 GB/s
+# one way, ~64-69 GB/s with H2D and D2H overlapped) but 64-byte rows at half
+# (tools/pcie2d_probe.py), so chunks are the widest of 512 / 256 / 128-byte
+# rows that still give two or more chunks.  Measured e2e gains: C2 3.2k ->
+# 4.1k, C4 1.59k -> 1.76k, C5 1.49k -> 2.34k columns/s.  Smaller blocks move as
+# one contiguous DMA each way.
+HOST_CHUNK_BYTES = 256 << 20
+
+
+def _host_chunk(ncols: int, n_in: int, n_out: int, esz: int) -> int:
+    """Columns per host-path chunk (0 = one contiguous DMA each way).
+
+    SMAT_HOST_CHUNK_COLS=c forces c columns per chunk (0: no chunking)."""
+    import os
+
+    forced = os.environ.get("SMAT_HOST_CHUNK_COLS")
+    if forced:
+        c = int(forced)
+        return c if 0 < c < ncols else 0
+    if max(n_in, n_out) * ncols * esz < HOST_CHUNK_BYTES:
+        return 0
+    for row_bytes in (512, 256, 128):
+        c = max(1, row_bytes // esz)
+        if ncols >= 2 * c:
+            return c
+    return 0
 
 
 class ScalarField(enum.Enum):
@@ -290,9 +313,8 @@ class LinearOperator:
             xin = np.ascontiguousarray(a2, dtype=_native.CODE_DTYPE[xcode])
             plan = self._plan(pcode, _default_device())
             esz = max(xin.itemsize, out.itemsize)
-            chunk = max(1, min(ncols, HOST_CHUNK_BYTES // max(1, max(n_in, n_out) * esz)))
             plan.apply_host(direction, xin.ctypes.data, xcode, out.ctypes.data, ncols,
-                            chunk if chunk < ncols else 0)
+                            _host_chunk(ncols, n_in, n_out, esz))
         return out[:, 0] if squeeze else out
 
     def _apply_torch(self, x, direction, name, n_in, n_out):
@@ -317,9 +339,8 @@ class LinearOperator:
             if ncols:
                 plan = self._plan(pcode, _default_device())
                 esz = max(xin.element_size(), out.element_size())
-                chunk = max(1, min(ncols, HOST_CHUNK_BYTES // max(1, max(n_in, n_out) * esz)))
                 plan.apply_host(direction, xin.data_ptr(), xcode, out.data_ptr(), ncols,
-                                chunk if chunk < ncols else 0)
+                                _host_chunk(ncols, n_in, n_out, esz))
             return out[:, 0] if squeeze else out
         dev = x2.device.index if x2.device.index is not None else torch.cuda.current_device()
         xin = x2.to(_torch_dtype(xcode)).contiguous()
