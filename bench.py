@@ -51,7 +51,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg", "ista"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -554,6 +554,78 @@ def run_solver(args):
         dist.destroy_process_group()
 
 
+def _ista_problem(size: int, seed: int = 1710):
+    """The reference bench's ISTA scenario (pkg/src/linopkit/bench.py:142-162)
+    restated: Partial(Hadamard(log2 m), rows) . Circulant(c), m = 2 size,
+    size/16-sparse truth; returns (operator factors, b, lam) in numpy."""
+    rng = np.random.default_rng([seed, size])
+    m = 2 * size
+    rows = rng.choice(m, size=size, replace=False)
+    c = rng.standard_normal(m) / np.sqrt(m)
+    xt = np.zeros(m)
+    sup = rng.choice(m, size=max(1, size // 16), replace=False)
+    xt[sup] = rng.standard_normal(sup.size) + np.sign(rng.standard_normal(sup.size))
+    return rows, c, xt
+
+
+def run_ista(args):
+    """--workload ista: the reference bench's ISTA scenario at size 2^20
+    (Partial(Hadamard(21), 2^20 rows) . Circulant(2^21), float64), a fixed step
+    size, `--steps` ISTA iterations on the device (one CUDA graph replayed).
+    value = ISTA iterations per second."""
+    import torch
+
+    import paper_1710_09578_b200 as sm
+    from paper_1710_09578_b200 import solvers
+
+    torch.cuda.set_device(0)
+    size = 1 << 20
+    rows, c, xt = _ista_problem(size)
+    order = int(np.log2(2 * size))
+    op = sm.Product(sm.Partial(sm.Hadamard(order), row_indices=rows), sm.Circulant(c))
+    b = op.forward(xt)
+    lam = 0.02 * float(np.abs(op.backward(b)).max())
+    top = sm.power_iteration(op, mode="singular", tol=1e-6, max_iter=50, seed=0).value
+    alpha = 1.0 / (1.01 * top ** 2)
+    bd = torch.from_numpy(b).cuda()
+    sm.ista(op, bd, sm.IstaOptions(lam=lam, steps=max(1, args.warmup), step_size=alpha))  # warm-up + capture
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        res = sm.ista(op, bd, sm.IstaOptions(lam=lam, steps=args.steps, step_size=alpha))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_it = ev0.elapsed_time(ev1) / args.steps
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import linop_oracle as orc
+
+        oo = orc.product(orc.partial(orc.hadamard(order), rows), orc.circulant(c))
+        its = 2
+        t0 = time.perf_counter()
+        orc.ista(oo, b, lam, steps=its, step_size=alpha)
+        dt = time.perf_counter() - t0
+        cpu = {"value": its / dt, "unit": "iterations/s", "cores": 1, "kind": "port",
+               "sample": f"{its} ISTA iterations (+1 residual), numpy oracle of solvers.py:163-194 ({dt:.2f} s)"}
+    line = {
+        "metric": "ISTA iterations/s (reference bench ista scenario)", "value": 1e3 / ms_it,
+        "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_it,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, reference bench.py:142-162 shapes)",
+        "config": {"workload": "ista(Partial(Hadamard(21), 2^20 rows) . Circulant(2^21)), size 2^20",
+                   "step": "one ISTA iteration: forward, residual, backward, soft-threshold update",
+                   "graph": solvers.last_loop_mode},
+        "final_objective": float(res.objective_trace[-1]),
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def w_dtype(cfg):
     return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
 
@@ -562,6 +634,9 @@ def main():
     args = _args()
     if args.workload == "cg":
         run_solver(args)
+        return
+    if args.workload == "ista":
+        run_ista(args)
         return
     cfg = int(args.workload[1])
     if args.impl == "reference":

@@ -570,9 +570,30 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
 // y_rows mask the global row r = l + 2^lo*m + 2^(lo+w)*h: zero-pad rows
 // r >= x_rows on load (first pass only, lo == 0) and skip rows r >= y_rows on
 // store (last pass only, lo + w == order) — Partial(Hadamard, arange, arange).
+// Fused row selection of a pass: rows of the transform come from / go to rows
+// of a compact block through an int32 map (Partial with unique indices).
+struct RowMaps {
+  const int32_t* in = nullptr;   // first pass: transform row -> compact x row (-1: zero)
+  int64_t in_rs = 0;
+  const int32_t* out = nullptr;  // last pass: transform row -> compact y row (-1: skip)
+  int64_t out_rs = 0;
+};
+
 static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& x, const Blk& y,
-                     bool acc, int64_t x_rows, int64_t y_rows) {
+                     bool acc, int64_t x_rows, int64_t y_rows, const RowMaps& maps = RowMaps{}) {
   WhtArgs a;
+  const int64_t full = int64_t(1) << order;
+  if (lo == 0 && maps.in) {
+    a.in_map = maps.in;
+    a.in_rs = maps.in_rs;
+    x_rows = full;  // (every transform row has a map entry)
+  }
+  if (lo + w == order && maps.out) {
+    a.out_map = maps.out;
+    a.out_rs = maps.out_rs;
+    y_rows = full;
+  }
+  a.map_k = g.inner;
   const int64_t hi_cnt = int64_t(1) << (order - lo - w);
   a.x = x.p; a.y = y.p;
   a.xs1 = x.s1; a.xs2 = x.s2; a.xsi = x.si;
@@ -607,8 +628,10 @@ static void wht_pass(Ctx& c, int order, int lo, int w, const Geo& g, const Blk& 
 // Hadamard of order `order` along the rows of x -> y; x has x_rows valid rows
 // (zero padding beyond), only the first y_rows rows of the result are written.
 static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_rows = INT64_MAX,
-                    int64_t y_rows = INT64_MAX) {
+                    int64_t y_rows = INT64_MAX, const RowMaps& maps = RowMaps{}) {
   const int64_t N = int64_t(1) << order;
+  SMAT_CHECK((!maps.in && !maps.out) || (g.n1 * g.n2 == 1 && N > 1), SMAT_UNSUPPORTED,
+             "fused row selection needs a single batch");
   if (x_rows >= N) x_rows = INT64_MAX;
   if (y_rows >= N) y_rows = INT64_MAX;
   if (N == 1) {
@@ -616,7 +639,7 @@ static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_
     return;
   }
   if (N <= kTileMax) {
-    wht_pass(c, order, 0, order, g, x, y, acc, x_rows, y_rows);
+    wht_pass(c, order, 0, order, g, x, y, acc, x_rows, y_rows, maps);
     return;
   }
   if (!merge_outer(g, x, y)) {
@@ -631,7 +654,7 @@ static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_
   for (int i = 0; i < order % npass; ++i) widths[i] += 1;
   const size_t m0 = c.mark();
   Blk T = y;
-  const bool y_ok = !acc && y.si == g.inner && y_rows == INT64_MAX;
+  const bool y_ok = !acc && y.si == g.inner && y_rows == INT64_MAX && !maps.out;
   if (!y_ok) T = c.alloc_blk(c.dt, g, N);
   int lo = 0;
   for (int p = 0; p < npass; ++p) {
@@ -639,7 +662,7 @@ static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_
     const Blk& src = p == 0 ? x : T;
     const Blk& dst = (last && !y_ok) ? y : T;
     wht_pass(c, order, lo, widths[p], g, src, dst, last && !y_ok ? acc : false, p == 0 ? x_rows : INT64_MAX,
-             last ? y_rows : INT64_MAX);
+             last ? y_rows : INT64_MAX, maps);
     lo += widths[p];
   }
   c.release(m0);
@@ -1261,14 +1284,37 @@ struct PartialNode : Node {
   // "Hadamard-padded" operator — zero-pad on load / truncate on store of the
   // FWHT passes, no scatter, gather or padded copies
   int had_order = -1;
+  // base is a Hadamard and every selection is duplicate-free: the selection
+  // is fused into the FWHT passes as int32 row maps (base row -> compact row,
+  // -1 = not selected) — gather on store, scatter on load, no extra passes
+  int map_order = -1;
+  DevBuf* rmap = nullptr;  // base rows -> selected row position
+  DevBuf* cmap = nullptr;  // base cols -> selected col position
   std::string describe() const override {
-    return std::string(had_order >= 0 ? "PaddedHadamard(" : "Partial(") + base->describe() + ")";
+    return std::string(had_order >= 0 ? "PaddedHadamard(" : map_order >= 0 ? "SelectedHadamard(" : "Partial(") +
+           base->describe() + ")";
   }
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
     const size_t m0 = c.mark();
     Blk x = promote(c, x0, g, adj ? rows : cols);
     if (had_order >= 0) {
       run_wht(c, had_order, g, x, y, acc, adj ? rows : cols, adj ? cols : rows);
+      c.release(m0);
+      return;
+    }
+    if (map_order >= 0 && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner) {
+      RowMaps m;
+      DevBuf* in = adj ? rmap : cmap;
+      DevBuf* out = adj ? cmap : rmap;
+      if (in) {
+        m.in = (const int32_t*)in->p;
+        m.in_rs = x.si;
+      }
+      if (out) {
+        m.out = (const int32_t*)out->p;
+        m.out_rs = y.si;
+      }
+      run_wht(c, map_order, g, x, y, acc, INT64_MAX, INT64_MAX, m);
       c.release(m0);
       return;
     }
@@ -1813,6 +1859,21 @@ struct Builder {
           if (bn.kind == SMAT_HADAMARD && (!nd.iparam[0] || is_prefix(nd.param[0])) &&
               (!nd.iparam[1] || is_prefix(nd.param[1])))
             a->had_order = int(bn.iparam[0]);
+          else if (bn.kind == SMAT_HADAMARD && bn.iparam[0] >= 1 && a->r_unique && a->c_unique &&
+                   (nd.iparam[0] || nd.iparam[1]) && !dt_int(p.dt)) {
+            // int32 row maps of the selections (reference composites.py:281-310)
+            const int64_t full = int64_t(1) << bn.iparam[0];
+            auto make_map = [&](const smat_param& prm) {
+              std::vector<int32_t> m(size_t(full), -1);
+              const int64_t* v = (const int64_t*)prm.data;
+              for (int64_t k = 0; k < prm.len; ++k) m[size_t(v[k])] = int32_t(k);
+              smat_param mp{m.data(), full, SMAT_I32, 0};
+              return upload_param(p, mp, SMAT_I32);
+            };
+            if (nd.iparam[0] && nd.param[0].dtype == SMAT_I64) a->rmap = make_map(nd.param[0]);
+            if (nd.iparam[1] && nd.param[1].dtype == SMAT_I64) a->cmap = make_map(nd.param[1]);
+            if ((!nd.iparam[0] || a->rmap) && (!nd.iparam[1] || a->cmap)) a->map_order = int(bn.iparam[0]);
+          }
         }
         out = a;
         break;

@@ -107,6 +107,11 @@ struct WhtDev {
   // two-level rows: (i & i_lo_mask) * si + (i >> i_lo_bits) * si_hi
   int32_t i_lo_bits, i_lo_mask;
   int64_t xsi_hi, ysi_hi;
+  // fused row selection (MASK instantiation only)
+  const int32_t* in_map;
+  const int32_t* out_map;
+  int64_t in_rs, out_rs;
+  int32_t map_k;
 };
 
 // b -> (o1, o2, c) with b = (o1*n2 + o2)*inner + c; returns the offset of the
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
   const uint32_t b = blockIdx.x * uint32_t(CT) + uint32_t(cs);
   const bool act = int32_t(b) < p.nb;
   int64_t xb = 0, yb = 0;
-  int32_t goff = 0;
+  int32_t goff = 0, mcol = 0;
   if (act) {
     uint32_t o1, o2, c;
     decode_batch(b, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c);
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
     if constexpr (MASK) {
       const uint32_t q = fdiv(b, p.gdiv.m, p.gdiv.s);
       goff = int32_t(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d) * p.g_mul;
+      mcol = int32_t(c % uint32_t(p.map_k));
     }
   }
   const T* x = (const T*)p.x + xb;
@@ -343,7 +349,15 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
     for (int r = 0; r < R0; ++r) {
       const int i = bb * R0 + r;
       bool ok = act;
-      if constexpr (MASK) ok = ok && goff + i * p.gin_stride < p.n_valid_in;
+      if constexpr (MASK) {
+        const int g = goff + i * p.gin_stride;
+        ok = ok && g < p.n_valid_in;
+        if (p.in_map) {
+          const int src = ok ? __ldg(&p.in_map[g]) : -1;
+          a[u * R0 + r] = src >= 0 ? ((const T*)p.x)[int64_t(src) * p.in_rs + mcol] : zero_of<T>();
+          continue;
+        }
+      }
       a[u * R0 + r] =
           ok ? x[int64_t(i & p.i_lo_mask) * p.xsi + int64_t(i >> p.i_lo_bits) * p.xsi_hi] : zero_of<T>();
     }
@@ -360,7 +374,15 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(T))) wht_tile_kernel(co
     for (int r = 0; r < RL; ++r) {
       const int k = base + r * NSL;
       if constexpr (MASK) {
-        if (goff + k * p.gout_stride >= p.n_valid_out) continue;
+        const int g = goff + k * p.gout_stride;
+        if (g >= p.n_valid_out) continue;
+        if (p.out_map) {
+          const int dst = __ldg(&p.out_map[g]);
+          if (dst < 0) continue;
+          T* yo = (T*)p.y + int64_t(dst) * p.out_rs + mcol;
+          *yo = p.acc ? *yo + a[u * RL + r] : a[u * RL + r];
+          continue;
+        }
       }
       const int64_t off = int64_t(k & p.i_lo_mask) * p.ysi + int64_t(k >> p.i_lo_bits) * p.ysi_hi;
       y[off] = p.acc ? y[off] + a[u * RL + r] : a[u * RL + r];
@@ -503,7 +525,12 @@ inline void wht_tile_launch(const WhtArgs& a, cudaStream_t s) {
   d.ysi_hi = a.i_lo_bits ? a.ysi_hi : 0;
   const int64_t gmax_in = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gin_stride;
   const int64_t gmax_out = (a.g_mod - 1) * a.g_mul + (N - 1) * a.gout_stride;
-  const bool mask = gmax_in >= a.n_valid_in || gmax_out >= a.n_valid_out;
+  const bool mask = gmax_in >= a.n_valid_in || gmax_out >= a.n_valid_out || a.in_map || a.out_map;
+  d.in_map = a.in_map;
+  d.out_map = a.out_map;
+  d.in_rs = a.in_rs;
+  d.out_rs = a.out_rs;
+  d.map_k = int32_t(a.map_k);
   if (mask) {
     SMAT_CHECK(fits31(gmax_in) && fits31(gmax_out), SMAT_UNSUPPORTED, "fwht tile: row index exceeds 2^31");
     d.gdiv = FastDiv(a.g_div);

@@ -72,6 +72,13 @@ struct WhtArgs {
   // (i >> i_lo_bits) * {x,y}si_hi when i_lo_bits > 0
   int32_t i_lo_bits = 0;
   int64_t xsi_hi = 0, ysi_hi = 0;
+  // row selection fused into the pass (Partial with unique indices): global
+  // input row g loads x[in_map[g] * in_rs + col] (zero where in_map[g] < 0),
+  // output row g stores to y[out_map[g] * out_rs + col] (skipped where < 0);
+  // col = (batch index % inner) % map_k.  Single-batch views only.
+  const int32_t* in_map = nullptr;
+  const int32_t* out_map = nullptr;
+  int64_t in_rs = 0, out_rs = 0, map_k = 1;
 };
 
 constexpr int kTileMax = 4096;

@@ -386,3 +386,26 @@ def test_c5_blocked_chain(N, K):
     X = (rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))) / np.sqrt(2)
     _close(op.forward(X), orc.apply(oo, X, 0), 1e-12, f"C5 blocked fwd N={N} K={K}")
     _close(op.backward(X), orc.apply(oo, X, 1), 1e-12, f"C5 blocked bwd N={N} K={K}")
+
+
+@pytest.mark.parametrize("order,K", [(6, 1), (10, 3), (13, 2), (21, 1)])
+def test_partial_hadamard_fused_selection(order, K):
+    """Partial(Hadamard) with unique arbitrary row / column selections runs as
+    FWHT passes with the selection fused (int32 row maps: gather on store,
+    scatter on load) and matches the oracle's scatter -> FWHT -> gather."""
+    rng = np.random.default_rng(order * 10 + K)
+    n = 1 << order
+    rows = rng.choice(n, size=n // 2, replace=False)
+    cols = rng.choice(n, size=n // 3 + 1, replace=False)
+    for r, c in ((rows, None), (None, cols), (rows, cols)):
+        op = sm.Partial(sm.Hadamard(order), r, c)
+        assert "SelectedHadamard" in op.plan_for(np.float64).describe()
+        oo = orc.partial(orc.hadamard(order), r, c)
+        x = rng.standard_normal((op.cols, K))
+        y = rng.standard_normal((op.rows, K))
+        _close(op.forward(x), orc.apply(oo, x, 0), 1e-12, f"partial H fwd order={order}")
+        _close(op.backward(y), orc.apply(oo, y, 1), 1e-12, f"partial H bwd order={order}")
+        if order <= 10:  # accumulate path (inside a Sum)
+            s = sm.Sum(op, sm.Dense(np.ones((op.rows, op.cols)) * 0.5))
+            so = orc.sum_(oo, orc.dense(np.ones((op.rows, op.cols)) * 0.5))
+            _close(s.forward(x), orc.apply(so, x, 0), 1e-12, "partial H in Sum")
