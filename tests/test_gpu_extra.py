@@ -194,3 +194,19 @@ def test_selfcheck_zoo_device():
     failed = [l for l in lines if l.startswith("FAIL")]
     assert not failed, "\n".join(failed)
     assert len(res) >= 50 and all(r.passed for r in res)
+
+
+def test_row_sharded_dft_device_single_rank():
+    """rowshard.sharded_dft with the device local steps (Kron(Identity,
+    Fourier) plans + Diagonal twiddles) on one rank: equals the oracle DFT."""
+    import torch
+
+    from paper_1710_09578_b200 import rowshard
+
+    rng = np.random.default_rng(9)
+    for nt, k in ((1 << 12, 2), (1 << 17, 3)):
+        x = rng.standard_normal((nt, k)) + 1j * rng.standard_normal((nt, k))
+        y = rowshard.sharded_dft(torch.from_numpy(x).cuda(), nt).cpu().numpy()
+        assert rel_l2(y, orc.dft(x)) < 1e-12
+        z = rowshard.sharded_dft(torch.from_numpy(y).cuda(), nt, inverse=True).cpu().numpy()
+        assert rel_l2(z, x) < 1e-12

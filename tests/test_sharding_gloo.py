@@ -71,3 +71,62 @@ def test_gloo_world2_shard_gather_and_max():
     assert all(ok for _, ok, _, _ in res)
     assert all(t == 2.0 for _, _, t, _ in res)  # max over ranks
     assert sorted(w for *_, w in res) == [3, 4]  # 7 columns split 4 + 3
+
+
+class _NumpyLocalOps:
+    """CPU stand-in for the device local steps of rowshard.sharded_dft (the
+    gloo test checks the all-to-all bookkeeping; the device steps are checked
+    on the GPU in tests/test_gpu_extra.py)."""
+
+    def fft_rows(self, x, a, n, inverse):
+        import torch
+
+        arr = x.numpy().reshape(a, n, -1)
+        f = np.fft.ifft(arr, axis=1) * n if inverse else np.fft.fft(arr, axis=1)
+        return torch.from_numpy(np.ascontiguousarray(f.reshape(a * n, -1)))
+
+    def scale_rows(self, x, w, key):
+        import torch
+
+        return x * torch.from_numpy(w)[:, None]
+
+
+def _rowshard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_09578_b200 import rowshard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        nt, k = 1 << 10, 3
+        x = rng.standard_normal((nt, k)) + 1j * rng.standard_normal((nt, k))
+        xl = torch.from_numpy(np.ascontiguousarray(rowshard.local_rows(x, rank, world)))
+        ops = _NumpyLocalOps()
+        y = rowshard.sharded_dft(xl, nt, ops=ops).numpy()
+        ok_f = bool(np.allclose(y, rowshard.local_rows(np.fft.fft(x, axis=0), rank, world), atol=1e-9))
+        z = rowshard.sharded_dft(torch.from_numpy(y), nt, inverse=True, ops=ops).numpy()
+        ok_i = bool(np.allclose(z, rowshard.local_rows(x, rank, world), atol=1e-12))
+        q.put((rank, ok_f, ok_i))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_gloo_world2_row_sharded_dft():
+    """Row-sharded four-step DFT (rowshard.py, §8(f) row 4): three
+    all-to-alls over gloo with world size 2 reproduce np.fft on the gathered
+    column, forward and inverse."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rowshard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=100) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    assert all(f and i for _, f, i in res), res
