@@ -210,3 +210,34 @@ def test_row_sharded_dft_device_single_rank():
         assert rel_l2(y, orc.dft(x)) < 1e-12
         z = rowshard.sharded_dft(torch.from_numpy(y).cuda(), nt, inverse=True).cpu().numpy()
         assert rel_l2(z, x) < 1e-12
+
+
+def test_extra_edge_cases_device():
+    """Empty blocks, 1-D inputs, integer and single-precision inputs through the
+    §8(f) operators; reference dtype rules (core.py:63-73)."""
+    rng = np.random.default_rng(21)
+    tri = [(0, 1, 2.0), (2, 0, -1.0), (2, 0, 0.5), (1, 2, 3.0)]
+    S = sm.Sparse(3, 3, tri)
+    dense = np.zeros((3, 3))
+    for i, j, v in tri:
+        dense[i, j] += v
+    assert S.forward(np.zeros((3, 0))).shape == (3, 0)
+    xi = np.array([1, -2, 3], dtype=np.int32)
+    yi = S.forward(xi)
+    assert yi.dtype == np.float64 and np.allclose(yi, dense @ xi)
+    xf = rng.standard_normal(3).astype(np.float32)
+    assert np.allclose(S.backward(xf), dense.T @ xf, atol=1e-5)
+    P = sm.Polynomial(sm.Hadamard(3), [1.0, 2.0, 3.0])
+    Hm = np.array([[(-1) ** bin(i & j).count("1") for j in range(8)] for i in range(8)], dtype=float)
+    Pm = np.eye(8) + 2 * Hm + 3 * Hm @ Hm
+    v = rng.standard_normal(8)
+    assert np.allclose(P.forward(v), Pm @ v) and P.forward(v).shape == (8,)
+    assert np.allclose(P.backward(v.astype(np.complex128)), Pm.T @ v)
+    E0 = sm.Sparse(4, 5, [])
+    assert np.array_equal(E0.forward(np.ones((5, 2))), np.zeros((4, 2)))
+    assert np.array_equal(E0.backward(np.ones((4, 2))), np.zeros((5, 2)))
+    # solvers on 1-D and float32 right-hand sides return float64 (result_type with the field)
+    A = sm.Diag(np.array([2.0, 3.0, 4.0]))
+    r = sm.cg_solve(A, np.array([2.0, 3.0, 4.0], dtype=np.float32), sm.SolveOptions(assume_hermitian=True))
+    assert r.solution.dtype == np.float64 and np.allclose(r.solution, 1.0) and r.converged
+    assert sm.soft_threshold(np.array([1, -3, 0], dtype=np.int32), 1).dtype == np.float64
