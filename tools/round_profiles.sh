@@ -8,6 +8,8 @@ set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
 echo "smoke rc=$?"
+python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest gpu rc=$?"
 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 echo "bench default rc=$?"
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
@@ -22,6 +24,12 @@ python tools/prof_cg.py 4 > gpurun_out/plain_cg.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file gpurun_out/launches_cg.csv python tools/prof_cg.py 4 > gpurun_out/ncu_cg.log 2>&1
 echo "launches cg rc=$?"
+python bench.py --workload ista --steps 50 --warmup 3 > gpurun_out/bench_ista.json 2> gpurun_out/bench_ista.err
+echo "bench ista rc=$?"
+python tools/prof_ista.py 2 > gpurun_out/plain_ista.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_ista.csv python tools/prof_ista.py 2 > gpurun_out/ncu_ista.log 2>&1
+echo "launches ista rc=$?"
 for w in 2 1 3 4 5; do
   python tools/prof_c2.py $w 1 > gpurun_out/plain_c$w.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
