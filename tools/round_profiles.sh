@@ -6,6 +6,8 @@
 # Every ncu command runs only after the same program exited 0 without ncu.
 set -u
 mkdir -p gpurun_out
+# (ncu reports stay in /tmp: gpurun copies back at most 64 MiB of gpurun_out/)
+rm -f /tmp/full_c2.ncu-rep /tmp/full_c5.ncu-rep
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
 echo "smoke rc=$?"
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
@@ -38,11 +40,11 @@ for w in 2 1 3 4 5; do
 done
 python tools/prof_c2.py 2 1 > /dev/null 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:fft_tma_kernel -c 3 \
-      -o gpurun_out/full_c2 python tools/prof_c2.py 2 1 > gpurun_out/ncu_full_c2.log 2>&1
+      -o /tmp/full_c2 python tools/prof_c2.py 2 1 > gpurun_out/ncu_full_c2.log 2>&1
 echo "full c2 rc=$?"
 python tools/prof_c2.py 5 1 > /dev/null 2>&1 && \
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"fft_tma|wht_tile|lr_" -c 9 \
-      -o gpurun_out/full_c5 python tools/prof_c2.py 5 1 > gpurun_out/ncu_full_c5.log 2>&1
+      -o /tmp/full_c5 python tools/prof_c2.py 5 1 > gpurun_out/ncu_full_c5.log 2>&1
 echo "full c5 rc=$?"
-python tools/ncu_summary.py gpurun_out/full_c2.ncu-rep > gpurun_out/full_c2_summary.txt 2>&1
-python tools/ncu_summary.py gpurun_out/full_c5.ncu-rep > gpurun_out/full_c5_summary.txt 2>&1
+python tools/ncu_summary.py /tmp/full_c2.ncu-rep > gpurun_out/full_c2_summary.txt 2>&1
+python tools/ncu_summary.py /tmp/full_c5.ncu-rep > gpurun_out/full_c5_summary.txt 2>&1
