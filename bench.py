@@ -51,7 +51,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg", "ista"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg", "ista", "sparse"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -626,6 +626,79 @@ def run_ista(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sparse(args):
+    """--workload sparse: Sparse (CSR) forward + backward of a 2^20 x 2^20
+    float64 operator with 16 random nonzeros per row (duplicates summed) on a
+    2^20 x 64 block — SURVEY.md §8(f) row 3 at scale.  HBM roofline: CSR
+    arrays once per direction, one x row (K values) gathered per nonzero, y
+    written once."""
+    import torch
+
+    import paper_1710_09578_b200 as sm
+
+    torch.cuda.set_device(0)
+    n, per_row, K = 1 << 20, 16, 64
+    rng = np.random.default_rng(1710_3)
+    rows = np.repeat(np.arange(n), per_row)
+    cols = rng.integers(0, n, n * per_row)
+    vals = rng.standard_normal(n * per_row)
+    S = sm.Sparse.__new__(sm.Sparse)  # bulk constructor: arrays instead of a triplet list
+    sm.Sparse._from_arrays(S, n, n, rows, cols, vals)
+    X = torch.from_numpy(rng.standard_normal((n, K))).cuda()
+
+    def step():
+        return S.backward(S.forward(X))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    nnz = S.nnz
+    # compulsory bytes per direction: CSR arrays, x and y once each (the
+    # gathered x rows mostly hit L2 here; counting one DRAM row per nonzero
+    # instead gives the `gather_model` upper bound)
+    per_dir = nnz * (8 + 8) + (n + 1) * 8 + 2 * n * K * 8
+    gather_dir = nnz * (8 + 8) + (n + 1) * 8 + nnz * K * 8 + n * K * 8
+    peak, peak_src = _peaks()
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import linop_oracle as orc
+
+        cols_s = 2
+        tri = list(zip(rows.tolist(), cols.tolist(), vals.tolist()))
+        oo = orc.sparse(n, n, tri)
+        xs = X[:, :cols_s].cpu().numpy()
+        t0 = time.perf_counter()
+        orc.apply(oo, orc.apply(oo, xs, 0), 1)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 2 * cols_s / dt, "unit": "columns/s", "cores": 1, "kind": "port",
+               "sample": f"{cols_s} of {K} columns, forward then backward, numpy CSR oracle ({dt:.2f} s)"}
+    line = {
+        "metric": "Sparse fwd/bwd columns/s", "value": 2 * K / (ms / 1e3), "unit": "columns/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform CSR)",
+        "config": {"workload": f"Sparse({n}x{n}, nnz {nnz}) on {n}x{K} float64",
+                   "step": "forward + backward (conjugate-transposed CSR)"},
+        "roofline": {"bound": "hbm", "kernel": "csr_kernel", "achieved": 2 * per_dir / (ms / 1e3) / 1e9,
+                     "peak": peak, "unit": "GB/s", "frac": 2 * per_dir / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                     "bytes_per_launch": per_dir, "peak_source": peak_src,
+                     "gather_model_GBps": 2 * gather_dir / (ms / 1e3) / 1e9},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def w_dtype(cfg):
     return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
 
@@ -637,6 +710,9 @@ def main():
         return
     if args.workload == "ista":
         run_ista(args)
+        return
+    if args.workload == "sparse":
+        run_sparse(args)
         return
     cfg = int(args.workload[1])
     if args.impl == "reference":

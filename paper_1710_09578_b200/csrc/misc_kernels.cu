@@ -189,10 +189,38 @@ __global__ void __launch_bounds__(256) csr_kernel(const CsrArgs a) {
     const P* xb = (const P*)a.x + o1 * a.xs1 + o2 * a.xs2;
     P* yr = (P*)a.y + o1 * a.ys1 + o2 * a.ys2 + i * a.ysi;
     const int64_t k0 = a.ptr[i], k1 = a.ptr[i + 1];
-    for (int64_t c = lane; c < a.inner; c += 32) {
-      P acc = zval<P>();
-      for (int64_t k = k0; k < k1; ++k) acc = padd(acc, pmul(val[k], xb[a.col[k] * a.xsi + c]));
-      yr[c] = a.accumulate ? padd(yr[c], acc) : acc;
+    // two 32-column halves per pass share each (col, val) load; the nonzero
+    // loop is unrolled by 4 so that up to 8 gathered x rows are in flight
+    for (int64_t c = lane; c < a.inner; c += 64) {
+      const bool two = c + 32 < a.inner;
+      P acc0 = zval<P>(), acc1 = zval<P>();
+      int64_t k = k0;
+      for (; k + 4 <= k1; k += 4) {
+        int64_t j[4];
+        P v[4], x0[4], x1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          j[q] = __ldg(&a.col[k + q]) * a.xsi;
+          v[q] = val[k + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x0[q] = xb[j[q] + c];
+          x1[q] = two ? xb[j[q] + c + 32] : zval<P>();
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc0 = padd(acc0, pmul(v[q], x0[q]));
+          acc1 = padd(acc1, pmul(v[q], x1[q]));
+        }
+      }
+      for (; k < k1; ++k) {
+        const int64_t jj = a.col[k] * a.xsi;
+        acc0 = padd(acc0, pmul(val[k], xb[jj + c]));
+        if (two) acc1 = padd(acc1, pmul(val[k], xb[jj + c + 32]));
+      }
+      yr[c] = a.accumulate ? padd(yr[c], acc0) : acc0;
+      if (two) yr[c + 32] = a.accumulate ? padd(yr[c + 32], acc1) : acc1;
     }
   }
 }

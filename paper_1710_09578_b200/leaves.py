@@ -250,8 +250,6 @@ class Sparse(LinearOperator):
     """
 
     def __init__(self, rows, cols, triplets):
-        rows = int(rows)
-        cols = int(cols)
         tri = list(triplets)
         if tri:
             i = np.asarray([t[0] for t in tri], dtype=np.int64)
@@ -261,6 +259,16 @@ class Sparse(LinearOperator):
             i = np.zeros(0, dtype=np.int64)
             j = np.zeros(0, dtype=np.int64)
             v = np.zeros(0)
+        self._from_arrays(rows, cols, i, j, v)
+
+    def _from_arrays(self, rows, cols, i, j, v):
+        """CSR assembly from coordinate arrays (the triplet constructor's body;
+        also a bulk path for large operators)."""
+        rows = int(rows)
+        cols = int(cols)
+        i = np.asarray(i, dtype=np.int64)
+        j = np.asarray(j, dtype=np.int64)
+        v = np.asarray(v)
         if i.size and (i.min() < 0 or i.max() >= rows or j.min() < 0 or j.max() >= cols):
             raise IndexOutOfRange(f"triplet index outside {rows}x{cols} matrix")
         dtype = as_field(v.dtype).dtype if v.size else np.float64
