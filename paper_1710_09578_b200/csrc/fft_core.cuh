@@ -180,6 +180,24 @@ __device__ __forceinline__ double2 tw_mul(double2 a, const double2* tw, int t) {
   return cmul(a, TWS ? tw[t] : __ldg(&tw[t]));
 }
 
+// Staged stage twiddle of the TMA pass.  F2: a single-precision table of plain
+// float2 entries (8 bytes: half the shared-memory traffic of the quads, one
+// more instruction per multiply to form (-w.y, w.x)) — used by the spectrum
+// passes, whose FFT + IFFT make shared memory their tightest pipe; the other
+// passes keep the quads (C2 plain pass 188 -> 200 us with float2 entries).
+template <bool F2>
+__device__ __forceinline__ float2 st_tw_mul(float2 a, const float2* tw, int t) {
+  if constexpr (F2) {
+    const float2 w = tw[t];
+    const float2 p = __fmul2_rn(make_float2(a.x, a.x), w);
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x), p);
+  } else {
+    return tw_mul<true>(a, tw, t);
+  }
+}
+template <bool F2>
+__device__ __forceinline__ double2 st_tw_mul(double2 a, const double2* tw, int t) { return cmul(a, tw[t]); }
+
 // Spectrum entry i (plan layout: float4 quads for complex64, double2 for
 // complex128) as a plain complex value, and as the quad for cmul_q.
 __device__ __forceinline__ float2 ld_spec(const float2* mid, int64_t i) {
@@ -220,7 +238,8 @@ __host__ __device__ constexpr int st_twoff(int N, int E, int s, bool mirror) {
 // Thread (j, cs) of a tile holds, at stage s (radix R, stride NS), the inputs
 // of butterflies bb = j + u*TPC (u < E/R): elements bb + r*N/R.  Outputs go to
 // (bb/NS)*NS*R + bb%NS + r*NS.  `tw` is W_TWN^t (t < TWN).
-template <class C, int N, int E, int CT, bool MIR, int S, int LAY = 0, int TWN = 4096, bool TWS = false>
+template <class C, int N, int E, int CT, bool MIR, int S, int LAY = 0, int TWN = 4096, bool TWS = false,
+          bool TF2 = false>
 __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* __restrict__ tw) {
   constexpr int NST = st_count(N, E);
   if constexpr (S < NST) {
@@ -236,7 +255,7 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
           // staged shared table (see st_twoff)
           const int t0 = st_twoff(N, E, S, MIR) + k * (R - 1) - 1;
 #pragma unroll
-          for (int r = 1; r < R; ++r) a[u * R + r] = tw_mul<true>(a[u * R + r], tw, t0 + r);
+          for (int r = 1; r < R; ++r) a[u * R + r] = st_tw_mul<TF2>(a[u * R + r], tw, t0 + r);
         } else {
           constexpr int step = TWN / (NS * R);
           const int ks = k * step;
@@ -264,7 +283,7 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
 #pragma unroll
         for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[ex_row<LAY, SH>(bb + r * (N / R2)) * CT + cs];
       }
-      fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS>(a, sm, j, cs, tw);
+      fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS, TF2>(a, sm, j, cs, tw);
     }
   }
 }

@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       }
       C* dst = mir ? tws_mir : tws;
       if constexpr (sizeof(C) == 8) {
-        reinterpret_cast<float4*>(dst)[e] = __ldg(reinterpret_cast<const float4*>(p.tw) + t4096);
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p.tw) + t4096);
+        if constexpr (MID) dst[e] = make_float2(q.x, q.y);  // (plain entries, st_tw_mul<true>)
+        else reinterpret_cast<float4*>(dst)[e] = q;
       } else {
         dst[e] = __ldg(reinterpret_cast<const C*>(p.tw) + t4096);
       }
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
 #pragma unroll
       for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
     }
-    fft_stages<C, N, E, CT, false, 0, LAY, N, true>(a, buf, j, cs, tws);
+    fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
     if constexpr (MID) {
       constexpr int RF = st_radix(N, E, NST - 1, false);
       // the tile's spectrum slice landed in shared memory with the data
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
             a[u * RF + r] = conj(cmul(a[u * RF + r], sv));
           }
       }
-      fft_stages<C, N, E, CT, true, 0, LAY, N, true>(a, buf, j, cs, tws_mir);
+      fft_stages<C, N, E, CT, true, 0, LAY, N, true, MID>(a, buf, j, cs, tws_mir);
     }
     // all exchange reads of the landing buffer are done after this barrier
     __syncthreads();
