@@ -180,6 +180,13 @@ __device__ __forceinline__ double2 tw_mul(double2 a, const double2* tw, int t) {
   return cmul(a, TWS ? tw[t] : __ldg(&tw[t]));
 }
 
+// a * w for a plain float2 w on the packed FP32x2 pipe: FMUL2 + FFMA2 with
+// (-w.y, w.x) formed in registers
+__device__ __forceinline__ float2 cmul_f2(float2 a, float2 w) {
+  const float2 p = __fmul2_rn(make_float2(a.x, a.x), w);
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x), p);
+}
+
 // Staged stage twiddle of the TMA pass.  F2: a single-precision table of plain
 // float2 entries (8 bytes: half the shared-memory traffic of the quads, one
 // more instruction per multiply to form (-w.y, w.x)) — used by the spectrum
@@ -188,9 +195,7 @@ __device__ __forceinline__ double2 tw_mul(double2 a, const double2* tw, int t) {
 template <bool F2>
 __device__ __forceinline__ float2 st_tw_mul(float2 a, const float2* tw, int t) {
   if constexpr (F2) {
-    const float2 w = tw[t];
-    const float2 p = __fmul2_rn(make_float2(a.x, a.x), w);
-    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x), p);
+    return cmul_f2(a, tw[t]);
   } else {
     return tw_mul<true>(a, tw, t);
   }
@@ -198,12 +203,9 @@ __device__ __forceinline__ float2 st_tw_mul(float2 a, const float2* tw, int t) {
 template <bool F2>
 __device__ __forceinline__ double2 st_tw_mul(double2 a, const double2* tw, int t) { return cmul(a, tw[t]); }
 
-// Spectrum entry i (plan layout: float4 quads for complex64, double2 for
-// complex128) as a plain complex value, and as the quad for cmul_q.
-__device__ __forceinline__ float2 ld_spec(const float2* mid, int64_t i) {
-  const float4 q = __ldg(reinterpret_cast<const float4*>(mid) + i);
-  return make_float2(q.x, q.y);
-}
+// Spectrum entry i (plan layout: float2 / double2).
+__device__ __forceinline__ float2 ld_spec(const float2* mid, int64_t i) { return __ldg(mid + i); }
+
 __device__ __forceinline__ double2 ld_spec(const double2* mid, int64_t i) { return __ldg(mid + i); }
 
 // Exchange-buffer row map.  LAY == 0: padded rows (row + row/16, the buffer

@@ -215,12 +215,6 @@ __global__ void block_rows_kernel(const double2* a, double2* out, int64_t n, int
   }
 }
 
-__global__ void c128_to_quad_kernel(const double2* a, float4* b, int64_t n) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const float c = float(a[i].x), s = float(a[i].y);
-    b[i] = make_float4(c, s, -s, c);
-  }
-}
 
 // Per-tile (four-step) copy of a pre/post vector of length n for transforms of
 // length Nt > kTileMax; nullptr when the transform is a single tile.
@@ -239,8 +233,7 @@ static DevBuf* fourstep_vector(Plan& p, const DevBuf* v, int64_t n, int64_t Nt, 
 
 // A convolution spectrum as the plan stores it: four-step order when the
 // convolution runs four-step (so the middle pass reads it contiguously per
-// tile), then in the plan's complex precision — double2 for complex128 plans,
-// the (w.x, w.y, -w.y, w.x) quad layout of cmul_q for complex64 plans.
+// tile), then in the plan's complex precision (double2 / float2).
 static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
   DevBuf* s = src;
   if (fourstep(src->len, true, cdt)) {
@@ -250,11 +243,9 @@ static DevBuf* spectrum_for_plan(Plan& p, DevBuf* src, int cdt) {
     fourstep_perm_kernel<<<1184, 256>>>((const double2*)src->p, (double2*)s->p, N1, N2);
     SMAT_CUDA(cudaGetLastError());
   }
-  if (cdt == SMAT_C128) return s;
-  DevBuf* q = new_buf(p, SMAT_C128, s->len);  // 16 bytes per entry
-  c128_to_quad_kernel<<<1184, 256>>>((const double2*)s->p, (float4*)q->p, s->len);
-  SMAT_CUDA(cudaGetLastError());
-  return q;
+  // single precision: plain float2 entries (the passes form (-w.y, w.x)
+  // themselves: half the bytes of the quad layout per tile slice)
+  return narrow_c128(p, s, cdt);
 }
 
 // ------------------------------------------------------ view utilities -----

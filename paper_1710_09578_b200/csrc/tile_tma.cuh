@@ -40,7 +40,8 @@ struct TmaGeom {
   static constexpr int ROWB = CT * int(sizeof(C));                 // bytes per tile row
   static constexpr int LAY = ROWB >= 128 ? 1 : 128 / ROWB;          // exchange row permutation
   static constexpr size_t BUF = size_t(N) * CT * sizeof(C);         // one dense TMA box
-  static constexpr size_t SPB = MS ? size_t(N) * 16 : 0;           // the tile's spectrum slice
+  // the tile's spectrum slice (MS 1, plain entries) or pre / post slice (MS 2)
+  static constexpr size_t SPB = MS == 1 ? size_t(N) * sizeof(C) : MS ? size_t(N) * 16 : 0;
   // four-step twiddles: the tile's slice of a precomputed table, bulk-loaded
   // with the tile (TVSL; measured faster than assembling them per CTA from
   // the two-level table even where it costs a landing buffer: C2's twiddle
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   auto issue = [&](int t, int s) {
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
-    const uint32_t sb = MID ? uint32_t(N) * 16 : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
+    const uint32_t sb = MID ? uint32_t(N * sizeof(C)) : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
     // (a masked box moves only the ein rows every tile owns)
     mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
     tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       const size_t g = size_t(tile_goff(t));
       if (sb) {
         const unsigned char* src =
-            MID ? reinterpret_cast<const unsigned char*>(p.mid) + g * p.mid_gmul * 16
+            MID ? reinterpret_cast<const unsigned char*>(p.mid) + g * p.mid_gmul * sizeof(C)
                 : side_pre ? reinterpret_cast<const unsigned char*>(p.pre) + g * p.pre_gmul * sizeof(C)
                            : reinterpret_cast<const unsigned char*>(p.post) + g * p.post_gmul * sizeof(C);
         bulk_load(stage_spec(s), src, sb, &bars[s]);
@@ -332,17 +333,17 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       constexpr int RF = st_radix(N, E, NST - 1, false);
       // the tile's spectrum slice landed in shared memory with the data
       if constexpr (sizeof(C) == 8) {
-        // quad spectrum: conj(a*s) = conj(cmul_q(a, q)); conj(a*conj s) = cmul_q(conj a, q)
-        const float4* mq = reinterpret_cast<const float4*>(stage_spec(sidx));
+        // plain spectrum: conj(a*s) = conj(a s); conj(a*conj s) = conj(a) s
+        const float2* ms = reinterpret_cast<const float2*>(stage_spec(sidx));
         const bool mc = (f & F_MIDCONJ) != 0;
 #pragma unroll
         for (int u = 0; u < E / RF; ++u)
 #pragma unroll
           for (int r = 0; r < RF; ++r) {
             const int k = j + u * TPC + r * (N / RF);
-            const float4 q = mq[k];
+            const float2 w = ms[k];
             C v = a[u * RF + r];
-            a[u * RF + r] = mc ? cmul_q(conj(v), q) : conj(cmul_q(v, q));
+            a[u * RF + r] = mc ? cmul_f2(conj(v), w) : conj(cmul_f2(v, w));
           }
       } else {
         const C* mid = reinterpret_cast<const C*>(stage_spec(sidx));
