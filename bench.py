@@ -191,9 +191,18 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+            return self
+        # the timed region starts only once the sampler is producing lines
+        # (short regions, e.g. 20 steps of C2 = 27 ms, still get samples)
+        t0 = time.time()
+        while time.time() - t0 < 5.0:
+            if self.path.exists() and self.path.stat().st_size > 0:
+                break
+            time.sleep(0.01)
+        self.skip = self.path.read_text().count("\n") if self.path.exists() else 0
         return self
 
     def __exit__(self, *exc):
@@ -209,7 +218,11 @@ class ClockSampler:
             return None
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
+        lines = self.path.read_text().splitlines()
+        # samples taken after the timed region began (keep the last pre-region
+        # sample when the region was shorter than the sampling interval)
+        lines = lines[max(0, getattr(self, "skip", 0) - 1):]
+        for line in lines:
             f = [t.strip() for t in line.split(",")]
             if len(f) < 9:
                 continue
