@@ -284,6 +284,7 @@ class Plan:
         self.rows = op.rows
         self.cols = op.cols
         self._ws_cache: dict = {}
+        self._ws_lock = threading.Lock()
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -310,20 +311,27 @@ class Plan:
         return buf.value.decode()
 
     # -- device path ----------------------------------------------------------
-    def workspace(self, direction: int, ncols: int):
-        """Cached torch uint8 workspace for (direction, ncols) on the plan device."""
+    def workspace(self, direction: int, ncols: int, stream_handle: int | None = None):
+        """Cached torch uint8 workspace for (direction, ncols, stream) on the plan
+        device.  Keyed by stream: applies on one stream are ordered, applies on
+        different streams (e.g. from different threads) must not share scratch
+        (the reference's concurrent-apply contract, core.py:5-7)."""
         import torch
 
-        key = (direction, ncols)
-        ws = self._ws_cache.get(key)
-        if ws is None:
-            nbytes = self.workspace_bytes(direction, ncols)
-            ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
-            self._ws_cache[key] = ws
+        if stream_handle is None:
+            with torch.cuda.device(self.device):
+                stream_handle = torch.cuda.current_stream(self.device).cuda_stream
+        key = (direction, ncols, int(stream_handle))
+        with self._ws_lock:
+            ws = self._ws_cache.get(key)
+            if ws is None:
+                nbytes = self.workspace_bytes(direction, ncols)
+                ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
+                self._ws_cache[key] = ws
         return ws
 
     def apply_device(self, direction: int, x, x_code: int, y, ncols: int, stream_handle: int) -> None:
-        ws = self.workspace(direction, ncols)
+        ws = self.workspace(direction, ncols, stream_handle)
         check(
             self._lib.smat_apply(self.handle, direction, ctypes.c_void_p(x.data_ptr()), x_code,
                                  ctypes.c_void_p(y.data_ptr()), ncols, ctypes.c_void_p(ws.data_ptr()),
@@ -333,7 +341,7 @@ class Plan:
 
     def apply_profiled(self, direction: int, x, x_code: int, y, ncols: int, stream_handle: int):
         """One smat_apply with per-launch CUDA events: [(label, ms), ...]."""
-        ws = self.workspace(direction, ncols)
+        ws = self.workspace(direction, ncols, stream_handle)
         cap = 256
         ms = (ctypes.c_float * cap)()
         n = ctypes.c_int32()

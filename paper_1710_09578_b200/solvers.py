@@ -153,7 +153,9 @@ class _Applier:
         self.plan = op._plan(self.code, device)
         self.ncols = ncols
         for d in (0, 1):
-            self.plan.workspace(d, ncols)  # allocated before any graph capture
+            # (this stream's workspaces; the capture stream's are allocated
+            # inside the capture, from the graph's private pool)
+            self.plan.workspace(d, ncols)
 
     def __call__(self, direction, x, y):
         torch = _torch()

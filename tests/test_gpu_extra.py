@@ -241,3 +241,38 @@ def test_extra_edge_cases_device():
     r = sm.cg_solve(A, np.array([2.0, 3.0, 4.0], dtype=np.float32), sm.SolveOptions(assume_hermitian=True))
     assert r.solution.dtype == np.float64 and np.allclose(r.solution, 1.0) and r.converged
     assert sm.soft_threshold(np.array([1, -3, 0], dtype=np.int32), 1).dtype == np.float64
+
+
+def test_concurrent_applies_threads_streams():
+    """Operators are safe for concurrent shared apply (reference core.py:5-7):
+    four threads, each on its own CUDA stream, apply one operator (including
+    a forked Sum/LowRank plan) at once; results equal the sequential ones."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(31)
+    N = 4096
+    U = (rng.standard_normal((N, 4)) + 1j * rng.standard_normal((N, 4))) / N
+    V = (rng.standard_normal((N, 4)) + 1j * rng.standard_normal((N, 4))) / N
+    c = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    op = sm.Sum(sm.Circulant(c), sm.LowRank(U, V))
+    xs = [torch.from_numpy(rng.standard_normal((N, 8)) + 1j * rng.standard_normal((N, 8))).cuda() for _ in range(4)]
+    ref = [op.forward(x).cpu().numpy() for x in xs]
+    out = [None] * 4
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(20):
+                y = op.forward(xs[i])
+            s.synchronize()
+            out[i] = y.cpu().numpy()
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(4):
+        assert np.array_equal(out[i], ref[i]) or rel_l2(out[i], ref[i]) < 1e-13
