@@ -577,7 +577,8 @@ inline int tma_variant() {
 // These passes are issue-latency bound at 8 warps per SM (ncu: 26% issue
 // utilisation, 0.4 eligible warps per scheduler); the second CTA hides more
 // of it than the lost load lead costs (C5 outer passes 2.34 / 2.00 ->
-// 2.09 / 1.78 ms), despite ~300 B of register spills at 128 registers.
+// 2.09 / 1.78 ms); the masked twiddle variant C5 uses spills 16 B at 128
+// registers, the spectrum (MID) variants ~300 B, so those keep two buffers.
 inline int tma_c128_nb1() {
   static int v = -1;
   if (v < 0) {

@@ -409,3 +409,27 @@ def test_partial_hadamard_fused_selection(order, K):
             s = sm.Sum(op, sm.Dense(np.ones((op.rows, op.cols)) * 0.5))
             so = orc.sum_(oo, orc.dense(np.ones((op.rows, op.cols)) * 0.5))
             _close(s.forward(x), orc.apply(so, x, 0), 1e-12, "partial H in Sum")
+
+
+@pytest.mark.parametrize("N,K", [(5003, 4), (70001, 8)])
+def test_c5_blocked_chain_with_singular_values(N, K):
+    """LowRank(U, V, s) inside the blocked chain: diag(s) folded into the
+    cuBLAS expansion factors (plain and blocked-row copies) at plan time."""
+    rng = np.random.default_rng(N * 3 + K)
+    d1 = np.exp(2j * np.pi * rng.random(N))
+    d2 = np.exp(2j * np.pi * rng.random(N))
+    U = (rng.standard_normal((N, 8)) + 1j * rng.standard_normal((N, 8))) / np.sqrt(2 * N)
+    V = (rng.standard_normal((N, 8)) + 1j * rng.standard_normal((N, 8))) / np.sqrt(2 * N)
+    s = rng.standard_normal(8) + 1j * rng.standard_normal(8)
+    idx = np.arange(N)
+    order = (N - 1).bit_length()
+    op = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2),
+                    sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx), sm.LowRank(U, V, s)))
+    oo = orc.product(orc.diagonal(d1), orc.fourier(N), orc.diagonal(d2),
+                     orc.sum_(orc.hadamard_padded(N), orc.lowrank(U, V, s)))
+    X = (rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))) / np.sqrt(2)
+    _close(op.forward(X), orc.apply(oo, X, 0), 1e-12, "C5 chain with s fwd")
+    _close(op.backward(X), orc.apply(oo, X, 1), 1e-12, "C5 chain with s bwd")
+    lr = sm.LowRank(U, V, s)
+    _close(lr.forward(X), orc.apply(orc.lowrank(U, V, s), X, 0), 1e-12, "LowRank with s fwd")
+    _close(lr.backward(X), orc.apply(orc.lowrank(U, V, s), X, 1), 1e-12, "LowRank with s bwd")
