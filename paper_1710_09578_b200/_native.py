@@ -322,6 +322,9 @@ class Plan:
             with torch.cuda.device(self.device):
                 stream_handle = torch.cuda.current_stream(self.device).cuda_stream
         key = (direction, ncols, int(stream_handle))
+        ws = self._ws_cache.get(key)
+        if ws is not None:
+            return ws
         with self._ws_lock:
             ws = self._ws_cache.get(key)
             if ws is None:

@@ -117,12 +117,19 @@ def _is_torch(x) -> bool:
     return t.__module__.startswith("torch") and t.__name__ in ("Tensor", "Parameter")
 
 
+_TORCH_NP: dict = {}
+
+
 def _np_dtype(x):
     if _is_torch(x):
-        import torch
+        dt = _TORCH_NP.get(x.dtype)
+        if dt is None:
+            import torch
 
-        return np.dtype(torch.empty((), dtype=x.dtype).numpy().dtype) if x.dtype != torch.bfloat16 \
-            else np.dtype(np.float32)
+            dt = np.dtype(torch.empty((), dtype=x.dtype).numpy().dtype) if x.dtype != torch.bfloat16 \
+                else np.dtype(np.float32)
+            _TORCH_NP[x.dtype] = dt
+        return dt
     return np.asarray(x).dtype if not hasattr(x, "dtype") else np.dtype(x.dtype)
 
 
@@ -143,7 +150,16 @@ def coerce_array(x, name="x"):
 
 
 def _work_codes(op, xdt: np.dtype):
-    """(plan dtype code, input dtype code) for an input of numpy dtype xdt."""
+    """(plan dtype code, input dtype code) for an input of numpy dtype xdt
+    (memoised per operator and dtype: the tree is immutable)."""
+    memo = op.__dict__.setdefault("_codes_memo", {})
+    got = memo.get(xdt)
+    if got is None:
+        got = memo[xdt] = _work_codes_uncached(op, xdt)
+    return got
+
+
+def _work_codes_uncached(op, xdt: np.dtype):
     if (np.issubdtype(xdt, np.integer) and op._int_exact()
             and xdt in (np.dtype(np.int32), np.dtype(np.int64))):
         code = _native.DTYPE_CODE[xdt]
@@ -160,13 +176,18 @@ def _work_codes(op, xdt: np.dtype):
     return plan, xcode
 
 
-def _torch_dtype(code):
-    import torch
+_TORCH_OF_CODE: dict = {}
 
-    return {
-        _native.F32: torch.float32, _native.F64: torch.float64, _native.C64: torch.complex64,
-        _native.C128: torch.complex128, _native.I32: torch.int32, _native.I64: torch.int64,
-    }[code]
+
+def _torch_dtype(code):
+    if not _TORCH_OF_CODE:
+        import torch
+
+        _TORCH_OF_CODE.update({
+            _native.F32: torch.float32, _native.F64: torch.float64, _native.C64: torch.complex64,
+            _native.C128: torch.complex128, _native.I32: torch.int32, _native.I64: torch.int64,
+        })
+    return _TORCH_OF_CODE[code]
 
 
 def _default_device() -> int:
@@ -241,6 +262,9 @@ class LinearOperator:
 
     # -- native plans -----------------------------------------------------------
     def _plan(self, code: int, device: int):
+        plan = self.__dict__.get("_plans", {}).get((code, device))
+        if plan is not None:  # (plans are never replaced once built)
+            return plan
         lock = self.__dict__.setdefault("_plan_lock", threading.Lock())
         with lock:
             cache = self.__dict__.setdefault("_plans", {})
@@ -342,14 +366,19 @@ class LinearOperator:
                 plan.apply_host(direction, xin.data_ptr(), xcode, out.data_ptr(), ncols,
                                 _host_chunk(ncols, n_in, n_out, esz))
             return out[:, 0] if squeeze else out
-        dev = x2.device.index if x2.device.index is not None else torch.cuda.current_device()
-        xin = x2.to(_torch_dtype(xcode)).contiguous()
+        cur = torch.cuda.current_device()
+        dev = x2.device.index if x2.device.index is not None else cur
+        xdt_t = _torch_dtype(xcode)
+        xin = x2 if (x2.dtype == xdt_t and x2.is_contiguous()) else x2.to(xdt_t).contiguous()
         out = torch.empty((n_out, ncols), dtype=_torch_dtype(pcode), device=x2.device)
         if ncols:
             plan = self._plan(pcode, dev)
-            with torch.cuda.device(dev):
-                stream = torch.cuda.current_stream(dev)
-                plan.apply_device(direction, xin, xcode, out, ncols, stream.cuda_stream)
+            if dev == cur:
+                plan.apply_device(direction, xin, xcode, out, ncols, torch.cuda.current_stream().cuda_stream)
+            else:
+                with torch.cuda.device(dev):
+                    stream = torch.cuda.current_stream(dev)
+                    plan.apply_device(direction, xin, xcode, out, ncols, stream.cuda_stream)
         return out[:, 0] if squeeze else out
 
     # -- derived operations --------------------------------------------------------
