@@ -7,7 +7,7 @@
 set -u
 mkdir -p gpurun_out
 # (ncu reports stay in /tmp: gpurun copies back at most 64 MiB of gpurun_out/)
-rm -f /tmp/full_c2.ncu-rep /tmp/full_c5.ncu-rep
+rm -f /tmp/full_c2.ncu-rep /tmp/full_c3.ncu-rep /tmp/full_c4.ncu-rep /tmp/full_c5.ncu-rep
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
 echo "smoke rc=$?"
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
@@ -46,5 +46,12 @@ python tools/prof_c2.py 5 1 > /dev/null 2>&1 && \
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"fft_tma|wht_tile|lr_" -c 9 \
       -o /tmp/full_c5 python tools/prof_c2.py 5 1 > gpurun_out/ncu_full_c5.log 2>&1
 echo "full c5 rc=$?"
+for w in 3 4; do
+  python tools/prof_c2.py $w 1 > /dev/null 2>&1 && \
+    ncu --set full --import-source on --clock-control none -k regex:"fft_tma|fft_tile|wht_tile" -c 8 \
+        -o /tmp/full_c$w python tools/prof_c2.py $w 1 > gpurun_out/ncu_full_c$w.log 2>&1
+  echo "full c$w rc=$?"
+  python tools/ncu_summary.py /tmp/full_c$w.ncu-rep > gpurun_out/full_c${w}_summary.txt 2>&1
+done
 python tools/ncu_summary.py /tmp/full_c2.ncu-rep > gpurun_out/full_c2_summary.txt 2>&1
 python tools/ncu_summary.py /tmp/full_c5.ncu-rep > gpurun_out/full_c5_summary.txt 2>&1
