@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SMAT_ABI_VERSION 1
+#define SMAT_ABI_VERSION 2  /* 2: SPARSE / POLYNOMIAL node kinds, solver steps */
 
 #if defined(__GNUC__)
 #define SMAT_API __attribute__((visibility("default")))

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(_native.LIB_PATH))
     for name in declared:
         assert hasattr(lib, name), name
-    assert _native.load_library().smat_abi_version() == 1
+    assert _native.load_library().smat_abi_version() == 2
 
 
 def test_struct_layout_matches_header():
