@@ -24,6 +24,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libsmat.so"
+ABI_VERSION = 2  # SMAT_ABI_VERSION of include/smat.h
 
 # smat_dtype
 F32, F64, C64, C128, I32, I64 = range(6)
@@ -174,6 +175,9 @@ def load_library(path: str | Path | None = None):
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = restype
+        if lib.smat_abi_version() != ABI_VERSION:
+            raise NativeError(f"{p} has ABI version {lib.smat_abi_version()}, this package needs {ABI_VERSION}: "
+                              "rebuild it with `python -m paper_1710_09578_b200.build`")
         if path is None:
             _lib = lib
         return lib
