@@ -350,6 +350,10 @@ struct XformIO {
   // intermediate there, so neither outer pass walks 2 MB-page strides
   bool x_blk = false, y_blk = false;
   int64_t blk_n2b = 0;
+  // fused row selection (single-tile transforms only): see FftArgs::in_map
+  const int32_t* in_map = nullptr;
+  const int32_t* out_map = nullptr;
+  int64_t in_rs = 0, out_rs = 0;
 };
 
 static void xform_pass_common(FftArgs& a, Ctx& c) {
@@ -390,9 +394,12 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.post = io.post; a.post_conj = io.post_conj;
     a.conj_x = io.conj_x; a.conj_y = io.conj_y; a.inv = io.inv && !io.mid;
     a.scale = io.scale; a.accumulate = io.acc;
+    a.in_map = io.in_map; a.in_rs = io.in_rs;
+    a.out_map = io.out_map; a.out_rs = io.out_rs;
     c.fft(cdt, int(Nt), a);
     return;
   }
+  SMAT_CHECK(!io.in_map && !io.out_map, SMAT_UNSUPPORTED, "fused row selection needs a single-tile transform");
   SMAT_CHECK(Nt <= int64_t(kTileMax) * kTileMax, SMAT_UNSUPPORTED,
              "transform length " + std::to_string(Nt) + " exceeds the two-pass limit 2^24");
   if (!merge_outer(g, io.x, io.y)) {
@@ -1279,10 +1286,14 @@ struct PartialNode : Node {
   // is fused into the FWHT passes as int32 row maps (base row -> compact row,
   // -1 = not selected) — gather on store, scatter on load, no extra passes
   int map_order = -1;
+  int64_t map_fourier = 0;  // base is Fourier(n), n a power of two in one tile: maps in the FFT pass
   DevBuf* rmap = nullptr;  // base rows -> selected row position
   DevBuf* cmap = nullptr;  // base cols -> selected col position
   std::string describe() const override {
-    return std::string(had_order >= 0 ? "PaddedHadamard(" : map_order >= 0 ? "SelectedHadamard(" : "Partial(") +
+    return std::string(had_order >= 0     ? "PaddedHadamard("
+                       : map_order >= 0   ? "SelectedHadamard("
+                       : map_fourier > 0  ? "SelectedFourier("
+                                          : "Partial(") +
            base->describe() + ")";
   }
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
@@ -1306,6 +1317,27 @@ struct PartialNode : Node {
         m.out_rs = y.si;
       }
       run_wht(c, map_order, g, x, y, acc, INT64_MAX, INT64_MAX, m);
+      c.release(m0);
+      return;
+    }
+    if (map_fourier > 0 && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner && dt_complex(c.dt) &&
+        !fourstep(map_fourier, false, cplx_of(c.dt))) {
+      // Fourier(n) forward DFT / backward F^H (leaves.py:171-175) as one
+      // tile pass, selection fused into its load and store
+      XformIO io;
+      io.x = x; io.x_rows = map_fourier; io.y = y; io.y_rows = map_fourier; io.acc = acc;
+      io.inv = adj;
+      DevBuf* in = adj ? rmap : cmap;
+      DevBuf* out = adj ? cmap : rmap;
+      if (in) {
+        io.in_map = (const int32_t*)in->p;
+        io.in_rs = x.si;
+      }
+      if (out) {
+        io.out_map = (const int32_t*)out->p;
+        io.out_rs = y.si;
+      }
+      run_xform(c, map_fourier, g, io);
       c.release(m0);
       return;
     }
@@ -1850,10 +1882,12 @@ struct Builder {
           if (bn.kind == SMAT_HADAMARD && (!nd.iparam[0] || is_prefix(nd.param[0])) &&
               (!nd.iparam[1] || is_prefix(nd.param[1])))
             a->had_order = int(bn.iparam[0]);
-          else if (bn.kind == SMAT_HADAMARD && bn.iparam[0] >= 1 && a->r_unique && a->c_unique &&
-                   (nd.iparam[0] || nd.iparam[1]) && !dt_int(p.dt)) {
+          else if (((bn.kind == SMAT_HADAMARD && bn.iparam[0] >= 1) ||
+                    (bn.kind == SMAT_FOURIER && is_pow2(bn.rows) && bn.rows >= 2 && bn.rows <= kTileMax &&
+                     dt_complex(p.dt))) &&
+                   a->r_unique && a->c_unique && (nd.iparam[0] || nd.iparam[1]) && !dt_int(p.dt)) {
             // int32 row maps of the selections (reference composites.py:281-310)
-            const int64_t full = int64_t(1) << bn.iparam[0];
+            const int64_t full = bn.kind == SMAT_HADAMARD ? int64_t(1) << bn.iparam[0] : bn.rows;
             auto make_map = [&](const smat_param& prm) {
               std::vector<int32_t> m(size_t(full), -1);
               const int64_t* v = (const int64_t*)prm.data;
@@ -1863,7 +1897,10 @@ struct Builder {
             };
             if (nd.iparam[0] && nd.param[0].dtype == SMAT_I64) a->rmap = make_map(nd.param[0]);
             if (nd.iparam[1] && nd.param[1].dtype == SMAT_I64) a->cmap = make_map(nd.param[1]);
-            if ((!nd.iparam[0] || a->rmap) && (!nd.iparam[1] || a->cmap)) a->map_order = int(bn.iparam[0]);
+            if ((!nd.iparam[0] || a->rmap) && (!nd.iparam[1] || a->cmap)) {
+              if (bn.kind == SMAT_HADAMARD) a->map_order = int(bn.iparam[0]);
+              else a->map_fourier = bn.rows;
+            }
           }
         }
         out = a;

@@ -82,6 +82,9 @@ struct FftDev {
   int32_t i_lo_bits;
   double scale;
   uint32_t flags;
+  const int32_t* in_map;  // fused row selection (GEN variant)
+  const int32_t* out_map;
+  int64_t in_rs, out_rs;
 };
 // Element offset of row i (two-level when lo_bits > 0).
 __device__ __forceinline__ int64_t row_off(int i, int32_t si, int64_t si_hi, int lo_bits) {
@@ -199,8 +202,10 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
         const int i = j + u * TPC + r * (N / R0);
         C v = mk(R(0), R(0));
         const int g = goff + i * p.gin_stride;
-        if (act && (!(f & F_PAD) || g < p.n_valid_in)) {
-          const int64_t off = row_off(i, p.xsi, p.xsi_hi, p.i_lo_bits);
+        int src = 0;
+        if (p.in_map && act) src = __ldg(&p.in_map[g]);
+        if (act && (!(f & F_PAD) || g < p.n_valid_in) && src >= 0) {
+          const int64_t off = p.in_map ? int64_t(src) * p.in_rs : row_off(i, p.xsi, p.xsi_hi, p.i_lo_bits);
           v = (f & F_XREAL) ? mk(__ldg(&xr[off]), R(0)) : __ldg(&xc[off]);
           if (f & F_CONJX) v = conj(v);
           if (p.pre) {
@@ -287,14 +292,15 @@ __global__ void __launch_bounds__(tile_threads(N, sizeof(C)), tile_min_blocks(N,
         const int g = goff + k * p.gout_stride;
         C v = a[u * RL + r];
         if (!TW && pre_conj) v = conj(v);
-        if (act && (!(f & F_TRUNC) || g < p.n_valid_out)) {
+        const int dst = (p.out_map && act) ? __ldg(&p.out_map[g]) : 0;
+        if (act && (!(f & F_TRUNC) || g < p.n_valid_out) && dst >= 0) {
           if (p.post) {
             const C w = __ldg(&((const C*)p.post)[p.post_gmul ? goff * p.post_gmul + k : g]);
             v = (f & F_POSTCONJ) ? cmulc(v, w) : cmul(v, w);
           }
           if (f & F_CONJY) v = conj(v);
           if (f & F_SCALE) v = scl(v, sc);
-          const int64_t off = row_off(k, p.ysi, p.ysi_hi, p.i_lo_bits);
+          const int64_t off = p.out_map ? int64_t(dst) * p.out_rs : row_off(k, p.ysi, p.ysi_hi, p.i_lo_bits);
           if (f & F_YREAL) {
             yr[off] = (f & F_ACC) ? yr[off] + v.x : v.x;
           } else {
@@ -467,6 +473,10 @@ inline FftDev make_fft_dev(const FftArgs& a, int N) {
   if (goff) f |= F_GOFF;
   if (a.tw_on && a.tw_pre) f |= F_TWPRE;
   d.flags = f;
+  d.in_map = a.in_map;
+  d.out_map = a.out_map;
+  d.in_rs = a.in_rs;
+  d.out_rs = a.out_rs;
   return d;
 }
 
@@ -497,7 +507,7 @@ inline void fft_tile_launch(const FftArgs& a, cudaStream_t s) {
   const FftDev d = make_fft_dev(a, N);
   constexpr int CT = tile_CT(N, sizeof(C));
   const bool fast = (a.nb % CT) == 0 && !a.x_real && !a.y_real && !a.pre && !a.post && !a.accumulate &&
-                    !(d.flags & (F_PAD | F_TRUNC | F_TWPRE)) && a.i_lo_bits == 0;
+                    !(d.flags & (F_PAD | F_TRUNC | F_TWPRE)) && a.i_lo_bits == 0 && !a.in_map && !a.out_map;
   // (an input-side twiddle runs in the generic variant's load loop)
   const bool mid = a.mid != nullptr, tw = a.tw_on != 0 && !a.tw_pre;
   if (mid && tw) fft_tile_go2<C, N, true, true>(d, a.nb, fast, s);

@@ -53,6 +53,13 @@ struct FftArgs {
   // > 0, row i of x sits at (i % 2^b)*xsi + (i >> b)*xsi_hi, likewise for y
   int32_t i_lo_bits = 0;
   int64_t xsi_hi = 0, ysi_hi = 0;
+  // fused row selection (Partial with unique indices; per-tile kernel only):
+  // input row g loads x[in_map[g] * in_rs] (zero where < 0), output row g
+  // stores to y[out_map[g] * out_rs] (skipped where < 0), both offset by the
+  // batch's view origin
+  const int32_t* in_map = nullptr;
+  const int32_t* out_map = nullptr;
+  int64_t in_rs = 0, out_rs = 0;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).

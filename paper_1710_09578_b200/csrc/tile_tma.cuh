@@ -469,7 +469,7 @@ inline bool tma_store_enabled() {
 template <class C, int N, int EP, int NB, int CTO = 0>
 inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   using G = TmaGeom<C, N, EP, NB, false, false, CTO>;
-  if (a.x_real || a.y_real || a.accumulate) return false;
+  if (a.x_real || a.y_real || a.accumulate || a.in_map || a.out_map) return false;
   if (a.inner % G::CT != 0) return false;
   const FftDev d0 = make_fft_dev(a, N);
   const bool pad = (d0.flags & F_PAD) != 0, trunc = (d0.flags & F_TRUNC) != 0;

@@ -433,3 +433,27 @@ def test_c5_blocked_chain_with_singular_values(N, K):
     lr = sm.LowRank(U, V, s)
     _close(lr.forward(X), orc.apply(orc.lowrank(U, V, s), X, 0), 1e-12, "LowRank with s fwd")
     _close(lr.backward(X), orc.apply(orc.lowrank(U, V, s), X, 1), 1e-12, "LowRank with s bwd")
+
+
+@pytest.mark.parametrize("n,K,dt", [(64, 1, np.complex128), (1024, 3, np.complex128), (4096, 2, np.complex64),
+                                    (8192, 2, np.complex128)])
+def test_partial_fourier_fused_selection(n, K, dt):
+    """Partial(Fourier(n)) — the partial-Fourier compressed-sensing operator —
+    with unique selections: one FFT tile pass with the selection fused into
+    its load / store (n <= 4096); longer transforms keep the generic
+    scatter / gather path.  Matches the oracle."""
+    rng = np.random.default_rng(n + K)
+    rows = rng.choice(n, size=n // 3, replace=False)
+    cols = rng.choice(n, size=n // 2, replace=False)
+    tol = 1e-5 if dt == np.complex64 else 1e-12
+    for r, c in ((rows, None), (None, cols), (rows, cols)):
+        op = sm.Partial(sm.Fourier(n), r, c)
+        if n <= 4096:
+            assert "SelectedFourier" in op.plan_for(dt).describe()
+        oo = orc.partial(orc.fourier(n), r, c)
+        x = (rng.standard_normal((op.cols, K)) + 1j * rng.standard_normal((op.cols, K))).astype(dt)
+        y = (rng.standard_normal((op.rows, K)) + 1j * rng.standard_normal((op.rows, K))).astype(dt)
+        _close(op.forward(x), orc.apply(oo, x, 0), tol, f"partial F fwd n={n}")
+        _close(op.backward(y), orc.apply(oo, y, 1), tol, f"partial F bwd n={n}")
+        xr = rng.standard_normal((op.cols, K))  # real input to the complex operator
+        _close(op.forward(xr), orc.apply(oo, xr, 0), 1e-12, f"partial F real fwd n={n}")
