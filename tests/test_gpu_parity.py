@@ -457,3 +457,29 @@ def test_partial_fourier_fused_selection(n, K, dt):
         _close(op.backward(y), orc.apply(oo, y, 1), tol, f"partial F bwd n={n}")
         xr = rng.standard_normal((op.cols, K))  # real input to the complex operator
         _close(op.forward(xr), orc.apply(oo, xr, 0), 1e-12, f"partial F real fwd n={n}")
+
+
+def test_c5_chain_random_sizes():
+    """The C5-type chain over a spread of lengths (Bluestein single-tile and
+    four-step, blocked chain taken or not) and column counts: fwd / bwd vs the
+    oracle at 1e-12, and the adjoint identity."""
+    rng = np.random.default_rng(1710_5)
+    for N in (97, 1031, 4099, 12289, 40009, 131101):
+        K = int(rng.integers(1, 7))
+        d1 = np.exp(2j * np.pi * rng.random(N))
+        d2 = np.exp(2j * np.pi * rng.random(N))
+        r = int(rng.integers(1, 33))
+        U = (rng.standard_normal((N, r)) + 1j * rng.standard_normal((N, r))) / np.sqrt(2 * N)
+        V = (rng.standard_normal((N, r)) + 1j * rng.standard_normal((N, r))) / np.sqrt(2 * N)
+        idx = np.arange(N)
+        order = (N - 1).bit_length()
+        op = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2),
+                        sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx), sm.LowRank(U, V)))
+        oo = orc.chain_c5(N, d1, d2, U, V)
+        X = rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))
+        Y = rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))
+        fx, by = op.forward(X), op.backward(Y)
+        _close(fx, orc.apply(oo, X, 0), 1e-12, f"C5-type fwd N={N} K={K} r={r}")
+        _close(by, orc.apply(oo, Y, 1), 1e-12, f"C5-type bwd N={N} K={K} r={r}")
+        lhs, rhs = np.vdot(Y, fx), np.vdot(by, X)
+        assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(X) * np.linalg.norm(Y) * np.sqrt(N)
