@@ -25,6 +25,11 @@ bounded sample on the host), gpu_launches, clocks.
 --impl reference: times the reference algorithm's CPU implementation (the
 oracle port; the reference is pure Python and cannot be installed on the GPU
 box) with all host cores (one process per column), rank 0 only.
+
+SURVEY.md §8(f) rows, one JSON line each (not driver workloads):
+  --workload cg      device CG on C2's operator (normal equations, 64 rhs)
+  --workload ista    the reference bench's ISTA scenario at size 2^20
+  --workload sparse  Sparse (CSR) fwd + bwd, 2^20 x 2^20 with 16.8 M nonzeros
 """
 
 from __future__ import annotations
