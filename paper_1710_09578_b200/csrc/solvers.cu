@@ -14,7 +14,6 @@
 // Column reductions are deterministic: a fixed grid of row blocks writes
 // partial sums (one per row block and column), and the finalising kernel of
 // each step adds them in row-block order.
-#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -27,8 +26,6 @@ namespace {
 using namespace smat;
 
 // ---- real / complex helpers (C = double or double2)
-__device__ __forceinline__ double re_(double a) { return a; }
-__device__ __forceinline__ double re_(double2 a) { return a.x; }
 __device__ __forceinline__ double abs2_(double a) { return a * a; }
 __device__ __forceinline__ double abs2_(double2 a) { return a.x * a.x + a.y * a.y; }
 __device__ __forceinline__ double abs_(double a) { return fabs(a); }
