@@ -224,7 +224,54 @@ __global__ void __launch_bounds__(256) csr_kernel(const CsrArgs a) {
     }
   }
 }
+// Narrow blocks (fewer than 32 columns, e.g. the solvers' single vectors):
+// G = next_pow2(inner) lanes per row, 32 / G rows per warp, so a K = 1
+// matrix-vector product runs one row per lane instead of one per warp.
+template <class P>
+__global__ void __launch_bounds__(256) csr_narrow_kernel(const CsrArgs a, int G) {
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G, per = 32 / G;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = a.rows * a.nb_outer;
+  const P* val = (const P*)a.val;
+  for (int64_t w = warp * per + sub; w < total; w += nwarps * per) {
+    const int64_t i = w % a.rows, o = w / a.rows;
+    const int64_t o2 = o % a.n2, o1 = o / a.n2;
+    const P* xb = (const P*)a.x + o1 * a.xs1 + o2 * a.xs2;
+    P* yr = (P*)a.y + o1 * a.ys1 + o2 * a.ys2 + i * a.ysi;
+    const int64_t k0 = a.ptr[i], k1 = a.ptr[i + 1];
+    for (int64_t c = gl; c < a.inner; c += G) {
+      P acc = zval<P>();
+      int64_t k = k0;
+      for (; k + 4 <= k1; k += 4) {
+        int64_t j[4];
+        P v[4], xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          j[q] = __ldg(&a.col[k + q]) * a.xsi;
+          v[q] = val[k + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = xb[j[q] + c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = padd(acc, pmul(v[q], xv[q]));
+      }
+      for (; k < k1; ++k) acc = padd(acc, pmul(val[k], xb[a.col[k] * a.xsi + c]));
+      yr[c] = a.accumulate ? padd(yr[c], acc) : acc;
+    }
+  }
+}
+
 template <class P> static void csr_go(const CsrArgs& a, cudaStream_t s) {
+  if (a.inner < 32) {
+    int G = 1;
+    while (G < a.inner) G <<= 1;
+    const int64_t warps = (a.rows * a.nb_outer + (32 / G) - 1) / (32 / G);
+    int64_t b = (warps + 7) / 8;
+    if (b > 148 * 32) b = 148 * 32;
+    csr_narrow_kernel<P><<<unsigned(b < 1 ? 1 : b), 256, 0, s>>>(a, G);
+    return;
+  }
   int64_t warps = a.rows * a.nb_outer;
   int64_t b = (warps + 7) / 8;
   if (b > 148 * 32) b = 148 * 32;
