@@ -199,3 +199,22 @@ def test_operator_algebra_sugar():
     a, b = sm.Fourier(4), sm.Hadamard(2)
     assert isinstance(a @ b, sm.Product) and isinstance(a * b, sm.Product)
     assert isinstance(a + b, sm.Sum) and (a + b).field is sm.ScalarField.COMPLEX128
+
+
+def test_bench_reference_arm_json_cpu():
+    """`bench.py --impl reference` runs the reference algorithm's CPU port on
+    the host (no GPU needed) and prints the contract's JSON line."""
+    import json
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--workload", "c1",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
