@@ -218,3 +218,13 @@ def test_bench_reference_arm_json_cpu():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_cli_usage_errors_cpu():
+    """The verify subcommand's usage errors exit with 2 before touching the
+    device (reference cli.py:125-133, 136-148)."""
+    from paper_1710_09578_b200.__main__ import cli_main
+
+    assert cli_main(["verify", "--max-size", "0"]) == 2
+    assert cli_main(["bogus"]) == 2
+    assert cli_main([]) == 2

@@ -276,3 +276,9 @@ def test_concurrent_applies_threads_streams():
         t.join()
     for i in range(4):
         assert np.array_equal(out[i], ref[i]) or rel_l2(out[i], ref[i]) < 1e-13
+
+
+def test_cli_verify_device():
+    from paper_1710_09578_b200.__main__ import cli_main
+
+    assert cli_main(["verify", "--max-size", "16"]) == 0
