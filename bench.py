@@ -413,7 +413,9 @@ def run_native(args, cfg):
                     "traffic": _traffic(args.workload, dom),
                     "bytes_per_launch": pb, "avg_launch_ms": dom_avg_ms,
                     "share_of_step": dom_t / total if total else None,
-                    "peak_source": peak_src}
+                    "peak_source": peak_src,
+                    # the north star's "~8 TB/s" nominal B200 HBM3e peak
+                    "frac_vs_nominal_8000": achieved / 8000.0}
     if cfg == 3:
         # FP32-bound config: algorithmic FFT flops of the
         # length-8192 embedding with real-pair packing, whole step, against the
