@@ -29,6 +29,9 @@ using SetWsFn = int (*)(Handle, void*, size_t);
 using ZgemmFn = int (*)(Handle, int, int, int, int, int, const double2*, const double2*, int, const double2*, int,
                         const double2*, double2*, int);
 
+using GemmAny = int (*)(Handle, int, int, int, int, int, const void*, const void*, int, const void*, int,
+                        const void*, void*, int);
+
 struct Blas {
   bool ok = false;
   CreateFn create = nullptr;
@@ -36,6 +39,7 @@ struct Blas {
   SetWsFn set_ws = nullptr;
   ZgemmFn zgemm = nullptr;
   ZgemmFn zgemm3m = nullptr;
+  GemmAny sgemm = nullptr, dgemm = nullptr, cgemm = nullptr;
 };
 
 const Blas& blas() {
@@ -52,7 +56,10 @@ const Blas& blas() {
     b.set_ws = (SetWsFn)dlsym(h, "cublasSetWorkspace_v2");
     b.zgemm = (ZgemmFn)dlsym(h, "cublasZgemm_v2");
     b.zgemm3m = (ZgemmFn)dlsym(h, "cublasZgemm3m");
-    b.ok = b.create && b.set_stream && b.set_ws && b.zgemm && b.zgemm3m;
+    b.sgemm = (GemmAny)dlsym(h, "cublasSgemm_v2");
+    b.dgemm = (GemmAny)dlsym(h, "cublasDgemm_v2");
+    b.cgemm = (GemmAny)dlsym(h, "cublasCgemm_v2");
+    b.ok = b.create && b.set_stream && b.set_ws && b.zgemm && b.zgemm3m && b.sgemm && b.dgemm && b.cgemm;
   });
   return b;
 }
@@ -95,6 +102,36 @@ void blas_zgemm(int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t
   const int st = (gauss3m ? b.zgemm3m : b.zgemm)(h, opa, opb, int(m), int(n), int(k), &one, (const double2*)A,
                                                  int(lda), (const double2*)B, int(ldb), &beta, (double2*)C, int(ldc));
   SMAT_CHECK(st == 0, SMAT_CUDA_ERROR, "cublasZgemm failed with status " + std::to_string(st));
+}
+
+// Column-major C = op(A) op(B) + beta C in the plan dtype (float32, float64,
+// complex64, complex128): the Dense leaf's plain GEMM.
+void blas_gemm(int dt, int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
+               int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc) {
+  const Blas& b = blas();
+  SMAT_CHECK(b.ok, SMAT_UNSUPPORTED, "cuBLAS not available");
+  SMAT_CHECK(m < (int64_t(1) << 31) && n < (int64_t(1) << 31) && k < (int64_t(1) << 31), SMAT_UNSUPPORTED,
+             "gemm dimension exceeds int32");
+  Handle h = handle_for(device);
+  SMAT_CHECK(b.set_stream(h, s) == 0, SMAT_CUDA_ERROR, "cublasSetStream failed");
+  int st = 0;
+  if (dt == SMAT_F32) {
+    const float one = 1.f, beta = float(beta_re);
+    st = b.sgemm(h, opa, opb, int(m), int(n), int(k), &one, A, int(lda), B, int(ldb), &beta, C, int(ldc));
+  } else if (dt == SMAT_F64) {
+    const double one = 1.0, beta = beta_re;
+    st = b.dgemm(h, opa, opb, int(m), int(n), int(k), &one, A, int(lda), B, int(ldb), &beta, C, int(ldc));
+  } else if (dt == SMAT_C64) {
+    const float2 one = make_float2(1.f, 0.f), beta = make_float2(float(beta_re), 0.f);
+    st = b.cgemm(h, opa, opb, int(m), int(n), int(k), &one, A, int(lda), B, int(ldb), &beta, C, int(ldc));
+  } else if (dt == SMAT_C128) {
+    const double2 one = make_double2(1.0, 0.0), beta = make_double2(beta_re, 0.0);
+    st = b.zgemm(h, opa, opb, int(m), int(n), int(k), &one, (const double2*)A, int(lda), (const double2*)B,
+                 int(ldb), &beta, (double2*)C, int(ldc));
+  } else {
+    throw Error(SMAT_BAD_DTYPE, "gemm: unsupported dtype");
+  }
+  SMAT_CHECK(st == 0, SMAT_CUDA_ERROR, "cublas gemm failed with status " + std::to_string(st));
 }
 
 }  // namespace smat

@@ -101,6 +101,8 @@ struct LowRankArgs {
 // libcublas cannot be loaded (or SMAT_LR_BLAS=0)
 bool blas_available();
 void blas_warm(int device);
+void blas_gemm(int dt, int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
+               int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc);
 void blas_zgemm(int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
                 int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc, bool gauss3m);
 

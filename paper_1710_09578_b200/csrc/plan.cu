@@ -706,6 +706,15 @@ struct DenseNode : Node {
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
     const size_t m0 = c.mark();
     Blk x = promote(c, x0, g, adj ? rows : cols);
+    if (!dt_int(c.dt) && blas_available() && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner) {
+      // library GEMM on the row-major blocks viewed column-major:
+      //   forward  Y' (K x rows) = X' (K x cols) A^T     (A^T = A's memory, ld cols)
+      //   backward Y' (K x cols) = X' (K x rows) conj(A) = X' (A^T)^H
+      if (!adj) c.gemm_blas(0, 0, g.inner, rows, cols, x.p, x.si, A->p, cols, acc ? 1.0 : 0.0, y.p, y.si);
+      else c.gemm_blas(0, 2, g.inner, cols, rows, x.p, x.si, A->p, cols, acc ? 1.0 : 0.0, y.p, y.si);
+      c.release(m0);
+      return;
+    }
     GemmArgs a;
     a.A = A->p;
     a.lda = cols;
@@ -1697,6 +1706,7 @@ struct Builder {
         auto* n = add<DenseNode>();
         SMAT_CHECK(nd.param[0].len == nd.rows * nd.cols, SMAT_BAD_SHAPE, "dense entries size");
         n->A = upload_param(p, nd.param[0], p.dt);
+        if (!dt_int(p.dt) && blas_available()) blas_warm(p.device);
         out = n;
         break;
       }

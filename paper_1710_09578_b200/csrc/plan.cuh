@@ -133,6 +133,11 @@ struct Ctx {
     note(label);
     if (!measure) blas_zgemm(device, stream, opa, opb, m, n, k, A, lda, B, ldb, beta, C, ldc, gauss3m);
   }
+  void gemm_blas(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                 int64_t ldb, double beta, void* C, int64_t ldc) {
+    note("gemm_blas");
+    if (!measure) blas_gemm(dt, device, stream, opa, opb, m, n, k, A, lda, B, ldb, beta, C, ldc);
+  }
   void lr_contract(const LowRankArgs& a) {
     launches += launch_lowrank_contract(dt, a, device, stream, true);
     note("lowrank_contract");
