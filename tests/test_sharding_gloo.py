@@ -130,3 +130,16 @@ def test_gloo_world2_row_sharded_dft():
     for p in procs:
         p.join(timeout=30)
     assert all(f and i for _, f, i in res), res
+
+
+def test_rowshard_split_lengths():
+    from paper_1710_09578_b200 import rowshard
+
+    assert rowshard.split_lengths(1 << 10, 2) == (32, 32)
+    assert rowshard.split_lengths(1 << 21, 8) == (2048, 1024)
+    with pytest.raises(ValueError):
+        rowshard.split_lengths(1000, 2)
+    with pytest.raises(ValueError):
+        rowshard.split_lengths(16, 8)  # 4 x 4 does not split over 8 ranks
+    x = np.arange(24).reshape(12, 2)
+    assert np.array_equal(rowshard.local_rows(x, 1, 3), x[4:8])
