@@ -194,15 +194,6 @@ __global__ void vec_mul_kernel(const C* a, const C* b, C* o, int64_t n) {
     o[i] = cmul(a[i], b[i]);
 }
 
-// out[i][q] = a[i][q] * (conj?) s[q]   (rows x r, row-major)
-__global__ void scale_cols_kernel(const double2* a, const double2* sv, int conj_s, double2* out, int64_t rows,
-                                  int64_t r) {
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * r; e += int64_t(gridDim.x) * blockDim.x) {
-    double2 w = sv[e % r];
-    if (conj_s) w.y = -w.y;
-    out[e] = cmul(a[e], w);
-  }
-}
 // Blocked-row copy of a (n x r) row-major factor into P rows: logical row
 // t = n1 + N1*k2 at ((n1 / 64) * N2b + k2) * 64 + n1 % 64, zero for t >= n.
 __global__ void block_rows_kernel(const double2* a, double2* out, int64_t n, int64_t r, int64_t N1, int64_t N2b) {
@@ -760,7 +751,8 @@ struct LowRankNode : Node {
       SMAT_CHECK(!blk || adj, SMAT_UNSUPPORTED, "blocked contraction is the adjoint's");
       const int64_t n = blk ? Ub->len / r : (adj ? rows : cols);
       const void* F = blk ? Ub->p : (adj ? U : V)->p;
-      c.zgemm(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner, true, "zgemm3m_contract");
+      if (c.dt == SMAT_C128) c.zgemm(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner, true, "zgemm3m_contract");
+      else c.gemm_blas(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner);
       return;
     }
     LowRankArgs la;
@@ -778,7 +770,8 @@ struct LowRankNode : Node {
       SMAT_CHECK(!blk || !adj, SMAT_UNSUPPORTED, "blocked expansion is the forward's");
       const int64_t n = blk ? Ubs->len / r : (adj ? cols : rows);
       const void* G = blk ? Ubs->p : (adj ? Vs : Us)->p;
-      c.zgemm(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si, false, "zgemm_expand");
+      if (c.dt == SMAT_C128) c.zgemm(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si, false, "zgemm_expand");
+      else c.gemm_blas(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si);
       return;
     }
     LowRankArgs lb;
@@ -1718,19 +1711,28 @@ struct Builder {
         n->U = upload_param(p, nd.param[0], p.dt);
         n->V = upload_param(p, nd.param[1], p.dt);
         if (nd.param[2].len) n->s = upload_param(p, nd.param[2], p.dt);
-        if (p.dt == SMAT_C128 && blas_available() && n->r <= 32) {
+        if (dt_complex(p.dt) && blas_available() && n->r <= 32) {
           n->blas = true;
           blas_warm(p.device);
           n->Us = n->U;
           n->Vs = n->V;
           if (n->s) {
-            n->Us = new_buf(p, SMAT_C128, n->U->len);
-            n->Vs = new_buf(p, SMAT_C128, n->V->len);
-            scale_cols_kernel<<<1184, 256>>>((const double2*)n->U->p, (const double2*)n->s->p, 0,
-                                             (double2*)n->Us->p, nd.rows, n->r);
-            scale_cols_kernel<<<1184, 256>>>((const double2*)n->V->p, (const double2*)n->s->p, 1,
-                                             (double2*)n->Vs->p, nd.cols, n->r);
-            SMAT_CUDA(cudaGetLastError());
+            // U diag(s), V diag(conj s) formed in fp64 on the host, stored at
+            // the plan precision
+            auto scaled = [&](const smat_param& f, int64_t nrows, bool cj) {
+              auto hf = convert_host(f, SMAT_C128);
+              auto hs = convert_host(nd.param[2], SMAT_C128);
+              const std::complex<double>* fv = (const std::complex<double>*)hf.data();
+              const std::complex<double>* sv = (const std::complex<double>*)hs.data();
+              std::vector<std::complex<double>> o(size_t(nrows * n->r));
+              for (int64_t i = 0; i < nrows; ++i)
+                for (int64_t q = 0; q < n->r; ++q)
+                  o[size_t(i * n->r + q)] = fv[i * n->r + q] * (cj ? std::conj(sv[q]) : sv[q]);
+              smat_param prm{o.data(), nrows * n->r, SMAT_C128, 0};
+              return upload_param(p, prm, p.dt);
+            };
+            n->Us = scaled(nd.param[0], nd.rows, false);
+            n->Vs = scaled(nd.param[1], nd.cols, true);
           }
         }
         out = n;
