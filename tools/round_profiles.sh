@@ -20,7 +20,7 @@ for w in c1 c2 c3 c4 c5; do
   python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
   echo "bench $w rc=$?"
 done
-python bench.py --workload cg --steps 20 --warmup 4 > gpurun_out/bench_cg.json 2> gpurun_out/bench_cg.err
+python bench.py --workload cg --steps 60 --warmup 4 > gpurun_out/bench_cg.json 2> gpurun_out/bench_cg.err
 echo "bench cg rc=$?"
 python tools/prof_cg.py 4 > gpurun_out/plain_cg.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
