@@ -17,7 +17,6 @@ from pathlib import Path
 import numpy as np
 
 from .errors import (
-    ChainMismatch,
     DimensionMismatch,
     LinOpError,
     NotPowerOfTwo,
