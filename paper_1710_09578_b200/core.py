@@ -190,6 +190,13 @@ def _torch_dtype(code):
     return _TORCH_OF_CODE[code]
 
 
+def _raw_stream(torch, dev: int) -> int:
+    """The current CUDA stream handle of `dev` (torch's raw accessor when
+    present: the public current_stream() costs several microseconds)."""
+    fn = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return fn(dev) if fn is not None else torch.cuda.current_stream(dev).cuda_stream
+
+
 def _default_device() -> int:
     import torch
 
@@ -374,7 +381,7 @@ class LinearOperator:
         if ncols:
             plan = self._plan(pcode, dev)
             if dev == cur:
-                plan.apply_device(direction, xin, xcode, out, ncols, torch.cuda.current_stream().cuda_stream)
+                plan.apply_device(direction, xin, xcode, out, ncols, _raw_stream(torch, dev))
             else:
                 with torch.cuda.device(dev):
                     stream = torch.cuda.current_stream(dev)
