@@ -158,8 +158,10 @@ class _Applier:
             self.plan.workspace(d, ncols)
 
     def __call__(self, direction, x, y):
+        from .core import _raw_stream
+
         torch = _torch()
-        self.plan.apply_device(direction, x, self.xcode, y, self.ncols, torch.cuda.current_stream().cuda_stream)
+        self.plan.apply_device(direction, x, self.xcode, y, self.ncols, _raw_stream(torch, x.device.index))
 
 
 def _native_work(op, dtype):
