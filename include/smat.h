@@ -18,9 +18,12 @@
  * launches the plan's fused passes on a CUDA stream.  No torch types cross
  * this boundary: plain pointers, sizes and a `cudaStream_t` passed as void*.
  *
- * Layout: x and y are (rows, ncols) C-contiguous blocks — the numpy/torch
- * default used by the reference (core.py:128-149): element (i, col) at
- * i*ncols + col.  Columns are independent.
+ * Layout: x and y are (rows, ncols) blocks — by default row-major
+ * (SMAT_ROW_MAJOR, the numpy/torch C order the reference uses,
+ * core.py:128-149): element (i, col) at i*ld + col with a leading dimension
+ * ld >= ncols (ld = ncols: C-contiguous; ld > ncols: a column slice of a wider
+ * block, read and written in place).  SMAT_COL_MAJOR blocks (Fortran order,
+ * element (i, col) at col*ld + i) are accepted too.  Columns are independent.
  *
  * Ownership: callers own x, y and the workspace; the plan owns every device
  * parameter (spectra, twiddles, chirps, diagonals, dense factors).  A plan is
@@ -42,7 +45,7 @@
 extern "C" {
 #endif
 
-#define SMAT_ABI_VERSION 2  /* 2: SPARSE / POLYNOMIAL node kinds, solver steps */
+#define SMAT_ABI_VERSION 3  /* 3: leading dimensions + layout on apply, peak probe */
 
 #if defined(__GNUC__)
 #define SMAT_API __attribute__((visibility("default")))
@@ -60,6 +63,11 @@ typedef enum smat_status {
   SMAT_UNSUPPORTED = 6,  /* operator/size combination with no device path       */
   SMAT_OOM = 7           /* device allocation failed                             */
 } smat_status;
+
+typedef enum smat_layout {
+  SMAT_ROW_MAJOR = 0, /* element (i, col) at i*ld + col, ld >= ncols (0: ld = ncols) */
+  SMAT_COL_MAJOR = 1  /* element (i, col) at col*ld + i, ld >= rows  (0: ld = rows)  */
+} smat_layout;
 
 typedef enum smat_dtype {
   SMAT_F32 = 0,
@@ -151,9 +159,13 @@ SMAT_API int smat_plan_build(const smat_node* nodes, int32_t n_nodes, const int3
                     int32_t n_children, int32_t root, int32_t dtype, int32_t device,
                     smat_plan** out);
 
-/* Device workspace (bytes) one smat_apply of `ncols` columns needs. */
-SMAT_API int smat_workspace_bytes(const smat_plan* plan, int32_t direction, int64_t ncols,
-                         size_t* out_bytes);
+/* Device workspace (bytes) one smat_apply of `ncols` columns with leading
+ * dimensions ldx / ldy (0 = dense) in `layout` needs.  Row-major blocks with
+ * ld > ncols are transformed in place where every pass of the plan can
+ * address the strided rows; otherwise (and for SMAT_COL_MAJOR) the apply
+ * stages the block through the workspace with one device copy each way. */
+SMAT_API int smat_workspace_bytes(const smat_plan* plan, int32_t direction, int64_t ncols, int64_t ldx,
+                                  int64_t ldy, int32_t layout, size_t* out_bytes);
 
 /* y = A·x (direction 0, forward — core.py:128-149) or y = A^H·x (direction 1,
  * backward — core.py:151-167) on device buffers; asynchronous on `stream`,
@@ -161,17 +173,18 @@ SMAT_API int smat_workspace_bytes(const smat_plan* plan, int32_t direction, int6
  * and (rows, ncols) for direction 1, in the plan dtype except that a real
  * input to a complex plan may be passed with `x_dtype` = the matching real
  * dtype (it is promoted on load, core.py:145).  y is written in the plan
- * dtype. */
+ * dtype.  ldx / ldy / layout: see "Layout" above (x and y must not overlap). */
 SMAT_API int smat_apply(const smat_plan* plan, int32_t direction, const void* x, int32_t x_dtype,
-               void* y, int64_t ncols, void* workspace, size_t workspace_bytes,
-               void* stream);
+                        int64_t ldx, void* y, int64_t ldy, int64_t ncols, int32_t layout,
+                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* End-to-end application on HOST buffers (the reference's numpy-in/numpy-out
  * contract, core.py:128-149): pinned or pageable host x, host y.  Columns are
  * streamed through the device in chunks so that host->device copies, the
  * device passes and device->host copies overlap on separate streams. */
 SMAT_API int smat_apply_host(const smat_plan* plan, int32_t direction, const void* x_host,
-                    int32_t x_dtype, void* y_host, int64_t ncols, int32_t chunk_cols);
+                             int32_t x_dtype, int64_t ldx, void* y_host, int64_t ldy, int64_t ncols,
+                             int32_t layout, int32_t chunk_cols);
 
 /* smat_apply with a CUDA event recorded on `stream` before every launch and
  * after the last one; synchronises the stream and returns the duration (ms) and
@@ -198,6 +211,12 @@ SMAT_API void smat_plan_free(smat_plan* plan);
 SMAT_API const char* smat_last_error(void);
 
 SMAT_API int smat_abi_version(void);
+
+/* Arithmetic peak of device `device` in TFLOP/s, measured by a short
+ * register-only kernel: kind 0 DFMA (FP64 vector), 1 DMMA m8n8k4 (FP64 tensor
+ * core), 2 DFMA and DMMA warps side by side, 3 FFMA2 (packed FP32).  The
+ * compute-roofline denominators of bench.py. */
+SMAT_API int smat_probe_peak(int32_t kind, int32_t device, double* tflops);
 
 /* ---------------------------------------------------------------------------
  * Device-resident solver steps (pkg/src/linopkit/solvers.py).  Every vector is

@@ -23,7 +23,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libsmat.so"
-ABI_VERSION = 2  # SMAT_ABI_VERSION of include/smat.h
+ABI_VERSION = 3  # SMAT_ABI_VERSION of include/smat.h
 
 # smat_dtype
 F32, F64, C64, C128, I32, I64 = range(6)
@@ -43,6 +43,8 @@ DTYPE_CODE = {
 CODE_DTYPE = {v: k for k, v in DTYPE_CODE.items()}
 REAL_OF = {C64: F32, C128: F64}
 
+# smat_layout
+ROW_MAJOR, COL_MAJOR = 0, 1
 # status codes
 OK, BAD_SHAPE, NOT_POW2, BAD_DTYPE, CUDA_ERROR, BAD_ARG, UNSUPPORTED, OOM = range(8)
 
@@ -85,18 +87,20 @@ _SIGNATURES = {
          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)],
         ctypes.c_int,
     ),
+    "smat_probe_peak": ([ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "smat_workspace_bytes": (
-        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)],
+        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+         ctypes.POINTER(ctypes.c_size_t)],
         ctypes.c_int,
     ),
     "smat_apply": (
-        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
-         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
+         ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
         ctypes.c_int,
     ),
     "smat_apply_host": (
-        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
-         ctypes.c_int32],
+        [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
+         ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32],
         ctypes.c_int,
     ),
     "smat_apply_profiled": (
@@ -287,6 +291,7 @@ class Plan:
         self.rows = op.rows
         self.cols = op.cols
         self._ws_cache: dict = {}
+        self._ws_bytes: dict = {}
         self._ws_lock = threading.Lock()
 
     def __del__(self):
@@ -298,10 +303,15 @@ class Plan:
                 pass
             self.handle = None
 
-    def workspace_bytes(self, direction: int, ncols: int) -> int:
-        out = ctypes.c_size_t()
-        check(self._lib.smat_workspace_bytes(self.handle, direction, ncols, ctypes.byref(out)))
-        return int(out.value)
+    def workspace_bytes(self, direction: int, ncols: int, ldx: int = 0, ldy: int = 0,
+                        layout: int = ROW_MAJOR) -> int:
+        key = (direction, ncols, ldx, ldy, layout)
+        got = self._ws_bytes.get(key)
+        if got is None:
+            out = ctypes.c_size_t()
+            check(self._lib.smat_workspace_bytes(self.handle, direction, ncols, ldx, ldy, layout, ctypes.byref(out)))
+            got = self._ws_bytes[key] = int(out.value)
+        return got
 
     def launches(self, direction: int, ncols: int) -> int:
         out = ctypes.c_int64()
@@ -314,33 +324,38 @@ class Plan:
         return buf.value.decode()
 
     # -- device path ----------------------------------------------------------
-    def workspace(self, direction: int, ncols: int, stream_handle: int | None = None):
-        """Cached torch uint8 workspace for (direction, ncols, stream) on the plan
-        device.  Keyed by stream: applies on one stream are ordered, applies on
-        different streams (e.g. from different threads) must not share scratch
-        (the reference's concurrent-apply contract, core.py:5-7)."""
+    def workspace(self, direction: int, ncols: int, stream_handle: int | None = None, ldx: int = 0, ldy: int = 0,
+                  layout: int = ROW_MAJOR):
+        """Cached torch uint8 workspace for (direction, stream) on the plan
+        device, grown when a wider block needs more (never one buffer per
+        width).  Keyed by stream: applies on one stream are ordered (a buffer
+        replaced by a larger one is only reused by later work on the same
+        stream), applies on different streams (e.g. from different threads)
+        must not share scratch (the reference's concurrent-apply contract,
+        core.py:5-7)."""
         import torch
 
         if stream_handle is None:
             with torch.cuda.device(self.device):
                 stream_handle = torch.cuda.current_stream(self.device).cuda_stream
-        key = (direction, ncols, int(stream_handle))
+        need = max(1, self.workspace_bytes(direction, ncols, ldx, ldy, layout))
+        key = (direction, int(stream_handle))
         ws = self._ws_cache.get(key)
-        if ws is not None:
+        if ws is not None and ws.numel() >= need:
             return ws
         with self._ws_lock:
             ws = self._ws_cache.get(key)
-            if ws is None:
-                nbytes = self.workspace_bytes(direction, ncols)
-                ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
+            if ws is None or ws.numel() < need:
+                ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
                 self._ws_cache[key] = ws
         return ws
 
-    def apply_device(self, direction: int, x, x_code: int, y, ncols: int, stream_handle: int) -> None:
-        ws = self.workspace(direction, ncols, stream_handle)
+    def apply_device(self, direction: int, x, x_code: int, y, ncols: int, stream_handle: int, ldx: int = 0,
+                     ldy: int = 0, layout: int = ROW_MAJOR) -> None:
+        ws = self.workspace(direction, ncols, stream_handle, ldx, ldy, layout)
         check(
-            self._lib.smat_apply(self.handle, direction, ctypes.c_void_p(x.data_ptr()), x_code,
-                                 ctypes.c_void_p(y.data_ptr()), ncols, ctypes.c_void_p(ws.data_ptr()),
+            self._lib.smat_apply(self.handle, direction, ctypes.c_void_p(x.data_ptr()), x_code, ldx,
+                                 ctypes.c_void_p(y.data_ptr()), ldy, ncols, layout, ctypes.c_void_p(ws.data_ptr()),
                                  ws.numel(), ctypes.c_void_p(stream_handle)),
             "smat_apply",
         )
@@ -364,9 +379,17 @@ class Plan:
 
     # -- host path --------------------------------------------------------------
     def apply_host(self, direction: int, x_ptr: int, x_code: int, y_ptr: int, ncols: int,
-                   chunk_cols: int = 0) -> None:
+                   chunk_cols: int = 0, ldx: int = 0, ldy: int = 0, layout: int = ROW_MAJOR) -> None:
         check(
-            self._lib.smat_apply_host(self.handle, direction, ctypes.c_void_p(x_ptr), x_code,
-                                      ctypes.c_void_p(y_ptr), ncols, chunk_cols),
+            self._lib.smat_apply_host(self.handle, direction, ctypes.c_void_p(x_ptr), x_code, ldx,
+                                      ctypes.c_void_p(y_ptr), ldy, ncols, layout, chunk_cols),
             "smat_apply_host",
         )
+
+
+def probe_peak(kind: int, device: int = 0) -> float:
+    """Measured arithmetic peak in TFLOP/s (smat_probe_peak): 0 DFMA, 1 DMMA,
+    2 DFMA + DMMA side by side, 3 FFMA2."""
+    out = ctypes.c_double()
+    check(load_library().smat_probe_peak(kind, device, ctypes.byref(out)), "smat_probe_peak")
+    return float(out.value)

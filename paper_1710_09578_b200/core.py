@@ -197,6 +197,21 @@ def _raw_stream(torch, dev: int) -> int:
     return fn(dev) if fn is not None else torch.cuda.current_stream(dev).cuda_stream
 
 
+def _block_layout(s0: int, s1: int, rows: int, ncols: int):
+    """(leading dimension, smat layout) of a 2-D block with element strides
+    (s0, s1), or (-1, ROW_MAJOR) when it needs a dense copy first.  Dense
+    row-major blocks report ld 0."""
+    if ncols == 1 or s1 == 1:
+        ld = s0 if rows > 1 else ncols
+        if ld == ncols:
+            return 0, _native.ROW_MAJOR
+        if ld > ncols:
+            return ld, _native.ROW_MAJOR
+    if s0 == 1 and s1 >= rows:
+        return s1, _native.COL_MAJOR
+    return -1, _native.ROW_MAJOR
+
+
 def _default_device() -> int:
     import torch
 
@@ -341,11 +356,20 @@ class LinearOperator:
         ncols = a2.shape[1]
         out = np.empty((n_out, ncols), dtype=_native.CODE_DTYPE[pcode])
         if ncols:
-            xin = np.ascontiguousarray(a2, dtype=_native.CODE_DTYPE[xcode])
+            xin = a2 if a2.dtype == _native.CODE_DTYPE[xcode] else a2.astype(_native.CODE_DTYPE[xcode])
+            ld, layout = _block_layout(xin.strides[0] // xin.itemsize if xin.strides[0] % xin.itemsize == 0 else -1,
+                                       xin.strides[1] // xin.itemsize if xin.strides[1] % xin.itemsize == 0 else -1,
+                                       n_in, ncols)
+            if ld < 0:
+                xin = np.ascontiguousarray(xin)
+                ld, layout = 0, _native.ROW_MAJOR
+            if layout == _native.COL_MAJOR:  # the result keeps the input's (Fortran) layout
+                out = np.empty((n_out, ncols), dtype=out.dtype, order="F")
             plan = self._plan(pcode, _default_device())
             esz = max(xin.itemsize, out.itemsize)
             plan.apply_host(direction, xin.ctypes.data, xcode, out.ctypes.data, ncols,
-                            _host_chunk(ncols, n_in, n_out, esz))
+                            _host_chunk(ncols, n_in, n_out, esz) if layout == _native.ROW_MAJOR else 0,
+                            ldx=ld, layout=layout)
         return out[:, 0] if squeeze else out
 
     def _apply_torch(self, x, direction, name, n_in, n_out):
@@ -363,29 +387,41 @@ class LinearOperator:
         xdt = _np_dtype(x2)
         pcode, xcode = _work_codes(self, xdt)
         ncols = x2.shape[1]
+        xdt_t = _torch_dtype(xcode)
+        # strided views (column slices of a wider block, transposes) are
+        # handed to the engine with their leading dimension: no copy here
+        xin = x2 if x2.dtype == xdt_t else x2.to(xdt_t)
+        ld, layout = _block_layout(xin.stride(0), xin.stride(1), n_in, ncols)
+        if ld < 0:
+            xin = xin.contiguous()
+            ld, layout = 0, _native.ROW_MAJOR
+        def _out(**kw):
+            # the result keeps the input's layout (column-major in, column-major out)
+            if layout == _native.COL_MAJOR:
+                return torch.empty((ncols, n_out), dtype=_torch_dtype(pcode), **kw).t()
+            return torch.empty((n_out, ncols), dtype=_torch_dtype(pcode), **kw)
+
         if not x2.is_cuda:
             # host tensor: pinned (or pageable) memory through the pipelined host path
-            xin = x2.to(_torch_dtype(xcode)).contiguous()
-            out = torch.empty((n_out, ncols), dtype=_torch_dtype(pcode), pin_memory=xin.is_pinned())
+            out = _out(pin_memory=xin.is_pinned())
             if ncols:
                 plan = self._plan(pcode, _default_device())
                 esz = max(xin.element_size(), out.element_size())
                 plan.apply_host(direction, xin.data_ptr(), xcode, out.data_ptr(), ncols,
-                                _host_chunk(ncols, n_in, n_out, esz))
+                                _host_chunk(ncols, n_in, n_out, esz) if layout == _native.ROW_MAJOR else 0,
+                                ldx=ld, layout=layout)
             return out[:, 0] if squeeze else out
         cur = torch.cuda.current_device()
         dev = x2.device.index if x2.device.index is not None else cur
-        xdt_t = _torch_dtype(xcode)
-        xin = x2 if (x2.dtype == xdt_t and x2.is_contiguous()) else x2.to(xdt_t).contiguous()
-        out = torch.empty((n_out, ncols), dtype=_torch_dtype(pcode), device=x2.device)
+        out = _out(device=x2.device)
         if ncols:
             plan = self._plan(pcode, dev)
             if dev == cur:
-                plan.apply_device(direction, xin, xcode, out, ncols, _raw_stream(torch, dev))
+                plan.apply_device(direction, xin, xcode, out, ncols, _raw_stream(torch, dev), ldx=ld, layout=layout)
             else:
                 with torch.cuda.device(dev):
                     stream = torch.cuda.current_stream(dev)
-                    plan.apply_device(direction, xin, xcode, out, ncols, stream.cuda_stream)
+                    plan.apply_device(direction, xin, xcode, out, ncols, stream.cuda_stream, ldx=ld, layout=layout)
         return out[:, 0] if squeeze else out
 
     # -- derived operations --------------------------------------------------------

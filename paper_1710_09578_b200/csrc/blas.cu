@@ -9,8 +9,8 @@
 //
 // cuBLAS is resolved at run time (dlopen of libcublas.so.12 — the copy torch
 // has already loaded, else the toolkit's), so libsmat.so has no link-time
-// dependency on it; one handle per (thread, device), each with a fixed
-// workspace so that the calls are CUDA-graph capturable.
+// dependency on it; one handle per (thread, device) and a fixed workspace per
+// (thread, device, stream), so that the calls are CUDA-graph capturable.
 #include <dlfcn.h>
 
 #include <cstdlib>
@@ -71,12 +71,24 @@ Handle handle_for(int device) {
   const Blas& b = blas();
   Handle h = nullptr;
   SMAT_CHECK(b.create(&h) == 0, SMAT_CUDA_ERROR, "cublasCreate failed");
-  void* ws = nullptr;
-  constexpr size_t kWs = size_t(32) << 20;
-  SMAT_CUDA(cudaMalloc(&ws, kWs));  // lives as long as the handle (process)
-  SMAT_CHECK(b.set_ws(h, ws, kWs) == 0, SMAT_CUDA_ERROR, "cublasSetWorkspace failed");
   handles[device] = h;
   return h;
+}
+
+// Bind the handle to stream s with a workspace of its own: cublasSetStream
+// resets the handle to cuBLAS's default workspace pool, so the fixed
+// workspace is re-attached after every stream switch — one buffer per
+// (thread, device, stream), never shared by two streams that may run
+// concurrently (the pattern of PyTorch's handle pool).
+void bind_stream(Handle h, int device, cudaStream_t s) {
+  thread_local std::unordered_map<uint64_t, void*> ws_by_stream;
+  constexpr size_t kWs = size_t(32) << 20;
+  const Blas& b = blas();
+  SMAT_CHECK(b.set_stream(h, s) == 0, SMAT_CUDA_ERROR, "cublasSetStream failed");
+  const uint64_t key = uint64_t(uintptr_t(s)) * 64 + uint64_t(device);
+  void*& ws = ws_by_stream[key];
+  if (!ws) SMAT_CUDA(cudaMalloc(&ws, kWs));  // lives as long as the thread's handle (process)
+  SMAT_CHECK(b.set_ws(h, ws, kWs) == 0, SMAT_CUDA_ERROR, "cublasSetWorkspace failed");
 }
 }  // namespace
 
@@ -97,7 +109,7 @@ void blas_zgemm(int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t
   SMAT_CHECK(m < (int64_t(1) << 31) && n < (int64_t(1) << 31) && k < (int64_t(1) << 31), SMAT_UNSUPPORTED,
              "zgemm dimension exceeds int32");
   Handle h = handle_for(device);
-  SMAT_CHECK(b.set_stream(h, s) == 0, SMAT_CUDA_ERROR, "cublasSetStream failed");
+  bind_stream(h, device, s);
   const double2 one = make_double2(1.0, 0.0), beta = make_double2(beta_re, 0.0);
   const int st = (gauss3m ? b.zgemm3m : b.zgemm)(h, opa, opb, int(m), int(n), int(k), &one, (const double2*)A,
                                                  int(lda), (const double2*)B, int(ldb), &beta, (double2*)C, int(ldc));
@@ -113,7 +125,7 @@ void blas_gemm(int dt, int device, cudaStream_t s, int opa, int opb, int64_t m, 
   SMAT_CHECK(m < (int64_t(1) << 31) && n < (int64_t(1) << 31) && k < (int64_t(1) << 31), SMAT_UNSUPPORTED,
              "gemm dimension exceeds int32");
   Handle h = handle_for(device);
-  SMAT_CHECK(b.set_stream(h, s) == 0, SMAT_CUDA_ERROR, "cublasSetStream failed");
+  bind_stream(h, device, s);
   int st = 0;
   if (dt == SMAT_F32) {
     const float one = 1.f, beta = float(beta_re);

@@ -99,19 +99,24 @@ static DevBuf* narrow_c128(Plan& p, DevBuf* src, int cdt) {
 }
 
 // ------------------------------------------------------ side streams -------
+// One side stream per (device, caller stream): independent callers (threads
+// on their own streams, the host path's chunk streams, a stream being
+// captured into a CUDA graph) never share one, so a fork neither serialises
+// unrelated applies nor drags another caller's work into a capture.
 namespace {
 std::mutex g_side_mu;
-std::unordered_map<int, cudaStream_t> g_side;
+std::unordered_map<uint64_t, cudaStream_t> g_side;
 }  // namespace
 
 cudaStream_t Ctx::fork() {
   cudaStream_t side = nullptr;
   {
+    const uint64_t key = uint64_t(uintptr_t(stream)) * 64 + uint64_t(device);
     std::lock_guard<std::mutex> lk(g_side_mu);
-    auto it = g_side.find(device);
+    auto it = g_side.find(key);
     if (it == g_side.end()) {
       SMAT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      g_side[device] = side;
+      g_side[key] = side;
     } else {
       side = it->second;
     }
@@ -194,15 +199,15 @@ __global__ void vec_mul_kernel(const C* a, const C* b, C* o, int64_t n) {
     o[i] = cmul(a[i], b[i]);
 }
 
-// Blocked-row copy of a (n x r) row-major factor into P rows: logical row
-// t = n1 + N1*k2 at ((n1 / 64) * N2b + k2) * 64 + n1 % 64, zero for t >= n.
-__global__ void block_rows_kernel(const double2* a, double2* out, int64_t n, int64_t r, int64_t N1, int64_t N2b) {
-  const int64_t P = N1 * N2b;
+// U~ rows in the C5 blocked chain's A2 unit order: unit row g = T' 64 + b,
+// T' = k2 NWa + a, holds logical row a + NWa b + N1 k2 of Uw, scaled.
+__global__ void utilde_perm_kernel(const double2* Uw, double2* Ut, int64_t P, int64_t r, int64_t N1, int64_t NWa,
+                                   double scale) {
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < P * r; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = e / r, q = e % r;
-    const int64_t n1 = t % N1, k2 = t / N1;
-    const int64_t ph = ((n1 >> 6) * N2b + k2) * 64 + (n1 & 63);
-    out[ph * r + q] = t < n ? a[e] : make_double2(0.0, 0.0);
+    const int64_t g = e / r, q = e % r;
+    const int64_t Tp = g / 64, b = g % 64, k2 = Tp / NWa, a = Tp % NWa;
+    const double2 v = Uw[(a + NWa * b + N1 * k2) * r + q];
+    Ut[e] = make_double2(v.x * scale, v.y * scale);
   }
 }
 
@@ -403,10 +408,14 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     return;
   }
   const int64_t ic = g.inner, O = g.n2;
-  SMAT_CHECK(io.x.si == ic && io.y.si == ic, SMAT_UNSUPPORTED, "four-step FFT needs row-contiguous views");
   const int l = ilog2(Nt);
   const int64_t N1 = int64_t(1) << ((l + 1) / 2);
   const int64_t N2 = Nt / N1;
+  // (the blocked single-batch passes address user rows through their row
+  // stride, so strided column slices are transformed in place; the batched
+  // variant folds (n1, column) into one contiguous index)
+  SMAT_CHECK((O == 1 && N1 >= 128) || (io.x.si == ic && io.y.si == ic), SMAT_UNSUPPORTED,
+             "four-step FFT needs row-contiguous views");
   const TwPair tw = twiddle_pair(c.device, Nt, dbl);
   // plain inverse transform = conj(F conj(.)) spread over the passes
   bool conj_first = io.conj_x, conj_last = io.conj_y;
@@ -637,7 +646,9 @@ static void run_wht(Ctx& c, int order, Geo g, Blk x, Blk y, bool acc, int64_t x_
     });
     return;
   }
-  SMAT_CHECK(x.si == g.inner, SMAT_UNSUPPORTED, "multi-pass FWHT needs row-contiguous input");
+  // (the first pass reads any row stride; the later ones fold the low row
+  // bits with the columns into one contiguous index)
+  SMAT_CHECK(y.si == g.inner, SMAT_UNSUPPORTED, "multi-pass FWHT needs a row-contiguous output");
   const int npass = (order + 11) / 12;
   std::vector<int> widths(npass, order / npass);
   for (int i = 0; i < order % npass; ++i) widths[i] += 1;
@@ -725,60 +736,69 @@ struct DenseNode : Node {
 struct LowRankNode : Node {
   DevBuf *U = nullptr, *V = nullptr, *s = nullptr;
   int64_t r = 0;
-  // complex128 plans with cuBLAS: the expansion factors with the diagonal
-  // folded in (U diag(s), V diag(conj s); U / V themselves when s is absent)
-  // and, for the DFSumNode chain, blocked-row copies of U (P rows, zero past
-  // the operator's rows)
-  DevBuf *Us = nullptr, *Vs = nullptr, *Ub = nullptr, *Ubs = nullptr;
-  bool blas = false;
+  // complex128, rank <= 32: the factors in the padded row layouts of the
+  // tensor-core passes (wlr_pitch: c = contraction, e = expansion fragments)
+  DevBuf *Uc = nullptr, *Ue = nullptr, *Vc = nullptr, *Ve = nullptr;
+  // C5 blocked chain (DFSumNode): U~ = H_{N2b} U / N2b (the Hadamard's k2
+  // stages applied ahead), rows in the chain's A2 unit order, both layouts
+  DevBuf *Utc = nullptr, *Ute = nullptr;
   std::string describe() const override {
-    return "LowRank(rank " + std::to_string(r) + (blas ? ", cuBLAS ZGEMM" : "") + ")";
+    return "LowRank(rank " + std::to_string(r) + (r <= 32 ? ", FP64 tensor-core halves" : "") + ")";
   }
-  // tall-skinny rank-r kernels apply (complex plan, single batch, row-contiguous)
+  // tall-skinny rank-r kernels apply (complex plan, rank <= 32, single batch)
   bool split_ok(const Ctx& c, const Blk& x, const Blk& y, const Geo& g) const {
-    return dt_complex(c.dt) && x.dt == c.dt && r <= 32 && g.n1 * g.n2 == 1 && x.si == g.inner &&
-           y.si == g.inner;
+    (void)y;
+    return dt_complex(c.dt) && x.dt == c.dt && r <= 32 && g.n1 * g.n2 == 1;
   }
-  size_t w_bytes(const Ctx& c, const Geo& g) const { return size_t(r) * size_t(g.inner) * dt_size(c.dt); }
-  // W = F^H x (row-slab reduction)
-  // (rm_n1 / rm_n2b: x rows in a blocked four-step layout, LowRankArgs)
-  void contract(Ctx& c, bool adj, const Blk& x, const Geo& g, void* w, int64_t rm_n1 = 0,
-                int64_t rm_n2b = 0) const {
-    if (blas) {
-      // W' (K x r, column-major) = X' (K x rows) F'^H, F' = (r x rows); blocked
-      // rows: all P rows of the blocked block against the blocked copy of U
-      const bool blk = rm_n1 > 0;
-      SMAT_CHECK(!blk || adj, SMAT_UNSUPPORTED, "blocked contraction is the adjoint's");
-      const int64_t n = blk ? Ub->len / r : (adj ? rows : cols);
-      const void* F = blk ? Ub->p : (adj ? U : V)->p;
-      if (c.dt == SMAT_C128) c.zgemm(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner, true, "zgemm3m_contract");
-      else c.gemm_blas(0, 2, g.inner, r, n, x.p, x.si, F, r, 0.0, w, g.inner);
+  // scratch of one contraction: complex128 -> per-CTA partials + the three
+  // real W' tables; complex64 -> W (r x K)
+  size_t w_bytes(const Ctx& c, const Geo& g) const {
+    if (c.dt == SMAT_C128)
+      return ((wlr_partial_bytes(c.device, g.inner) + 255) & ~size_t(255)) + size_t(3) * 32 * g.inner * 8;
+    return size_t(r) * size_t(g.inner) * dt_size(c.dt);
+  }
+  static double* w3_of(const Ctx& c, void* w, int64_t K) {
+    return reinterpret_cast<double*>(static_cast<char*>(w) + ((wlr_partial_bytes(c.device, K) + 255) & ~size_t(255)));
+  }
+  // W = F^H x (F = V forward, U backward), diag(s) folded in (conj for the adjoint)
+  void contract(Ctx& c, bool adj, const Blk& x, const Geo& g, void* w) const {
+    const int64_t kin = adj ? rows : cols;
+    if (c.dt == SMAT_C128) {
+      WlrMode m;
+      m.nw = 1; m.con = true; m.exp = false; m.in = true; m.out = false;
+      WlrArgs a;
+      a.in.p = x.p; a.in.ld = x.si; a.in.rows = kin;
+      a.F = (adj ? Uc : Vc)->p; a.r = r;
+      a.nrows = kin; a.n_f = kin; a.n_out = 0; a.K = g.inner;
+      a.partial = w;
+      c.wlr(m, a, "lowrank_contract");
+      c.wlr_fin(w, r, g.inner, s ? s->p : nullptr, adj, w3_of(c, w, g.inner));
       return;
     }
     LowRankArgs la;
-    la.F = (adj ? U : V)->p; la.x = x.p; la.w = w; la.rows = adj ? rows : cols; la.r = r;
+    la.F = (adj ? U : V)->p; la.x = x.p; la.w = w; la.rows = kin; la.r = r;
     la.K = g.inner; la.ldx = x.si;
-    la.rm_n1 = rm_n1; la.rm_n2b = rm_n2b;
     c.lr_contract(la);
   }
-  // y (+)= G diag(s) W
-  void expand(Ctx& c, bool adj, const void* w, const Blk& y, const Geo& g, bool acc, int64_t rm_n1 = 0,
-              int64_t rm_n2b = 0) const {
-    if (blas) {
-      // Y' (K x rows) (+)= W' (K x r) G'  with G = U diag(s) / V diag(conj s)
-      const bool blk = rm_n1 > 0;
-      SMAT_CHECK(!blk || !adj, SMAT_UNSUPPORTED, "blocked expansion is the forward's");
-      const int64_t n = blk ? Ubs->len / r : (adj ? cols : rows);
-      const void* G = blk ? Ubs->p : (adj ? Vs : Us)->p;
-      if (c.dt == SMAT_C128) c.zgemm(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si, false, "zgemm_expand");
-      else c.gemm_blas(0, 0, g.inner, n, r, w, g.inner, G, r, acc ? 1.0 : 0.0, y.p, y.si);
+  // y (+)= G W' (G = U forward, V backward)
+  void expand(Ctx& c, bool adj, const void* w, const Blk& y, const Geo& g, bool acc) const {
+    const int64_t kout = adj ? cols : rows;
+    if (c.dt == SMAT_C128) {
+      WlrMode m;
+      m.nw = 1; m.con = false; m.exp = true; m.in = acc; m.out = true;
+      WlrArgs a;
+      a.in.p = y.p; a.in.ld = y.si; a.in.rows = kout;
+      a.y = y.p; a.yout.g_lo = 1; a.yout.ld = y.si;
+      a.F = (adj ? Ve : Ue)->p; a.r = r;
+      a.nrows = kout; a.n_out = kout; a.n_f = kout; a.K = g.inner;
+      a.w3 = w3_of(c, const_cast<void*>(w), g.inner);
+      c.wlr(m, a, "lowrank_expand");
       return;
     }
     LowRankArgs lb;
-    lb.F = (adj ? V : U)->p; lb.w = const_cast<void*>(w); lb.y = y.p; lb.rows = adj ? cols : rows; lb.r = r;
+    lb.F = (adj ? V : U)->p; lb.w = const_cast<void*>(w); lb.y = y.p; lb.rows = kout; lb.r = r;
     lb.K = g.inner; lb.ldy = y.si;
     lb.s = s ? s->p : nullptr; lb.s_conj = adj; lb.accumulate = acc;
-    lb.rm_n1 = rm_n1; lb.rm_n2b = rm_n2b;
     c.lr_expand(lb);
   }
   void apply(Ctx& c, bool adj, const Blk& x0, const Blk& y, const Geo& g, bool acc) override {
@@ -1067,57 +1087,93 @@ struct SumNode : Node {
 };
 
 // Diag·Fourier·Diag (Bluestein, four-step) · Sum(PaddedHadamard, LowRank) —
-// the BASELINE C5 chain — with the Sum's result (forward) / operand (backward)
-// kept in the blocked four-step row layout of the Bluestein transform
-// (XformIO::x_blk / y_blk): logical row r = n1 + N1*k2 (N1 = the middle-pass
-// length) lives at row ((n1 / 64) * N2b + k2) * 64 + n1 % 64 of a P-row block
-// (P = 2^order, N2b = P / N1).  The padded Hadamard H_P = H_{N2b} (x) H_{N1}
-// splits along the same index: pass A transforms n1 (N1 contiguous user rows,
-// written blocked), pass B transforms k2 (64-row-strided blocked rows on both
-// sides), so every HBM pass of the chain except the user-layout side of the
-// FFT's far pass walks contiguous 64-row blocks instead of 2-4 MB row strides
-// (each row in its own 2 MB page: translation-bound).  The
-// rank-r contraction runs on the side stream against the user-layout block;
-// the expansion addresses the blocked rows through LowRankArgs::rm_n1.
+// the BASELINE C5 chain.  The padded Hadamard H_P (P = 2^order rows, zero
+// padding / truncation at the operator's n rows) factors along the
+// Bluestein transform's four-step row index r = n1 + N1 k2 (N1 = the middle
+// pass length) as H_{N2b}(k2) (x) H_64(b) (x) H_NWa(a), n1 = a + NWa b:
+//
+//   forward   A1  x -> T1        H_NWa over a, rank-r contraction V^H x of the
+//                                input rows (wlr.cu: 64-row x all-column tiles,
+//                                FP64 tensor cores)
+//             A2  T1 -> T2       H_64 over b, + U~ W' on the output rows
+//             B   T2 -> T2'      H_{N2b} over k2 (the FWHT tile pass)
+//             Bluestein (Diag·F·Diag folded into its chirps) from T2' in the
+//             blocked four-step row layout of the transform
+//   backward  the mirror image: Bluestein -> T2' (blocked), B, A2 (with the
+//             U~^H contraction of its input rows), A1 (with the V W''
+//             expansion of its output rows)
+//
+// U~ = H_{N2b} U / N2b in A2's row order is built at plan time: adding U~ W'
+// ahead of the k2 stages adds U W' after them (the Hadamard is linear, and
+// H_{N2b}^2 = N2b I), and in the adjoint U^H z = U~^H (H_{N2b} z).  The
+// factor rows are read once per direction — every LowRank tile spans all
+// columns — instead of once per column group of a transform tile.
+// Blocked layout of T2 / T2' (the Bluestein side): logical row n1 + N1 k2 at
+// ((n1 / 64) N2b + k2) 64 + n1 % 64 (XformIO::x_blk / y_blk).  T1: unit rows
+// of A2, (k2 NWa + a) 64 + b.
 struct DFSumNode : Node {
   Node* fallback = nullptr;       // the generic Product (used when a view does not qualify)
   DiagFourierNode* df = nullptr;
   Node* hp = nullptr;             // PaddedHadamard term
   LowRankNode* lr = nullptr;
-  int64_t N1 = 0, N2 = 0, N2b = 0, P = 0, M = 0;
+  int64_t N1 = 0, N2 = 0, N2b = 0, P = 0, M = 0, NWa = 0;
   std::string describe() const override { return "BlockedChain(" + fallback->describe() + ")"; }
   bool accepts_real() const override { return false; }
   bool usable(const Ctx& c, const Blk& x, const Blk& y, const Geo& g, bool acc) const {
-    return !acc && c.dt == SMAT_C128 && g.n1 * g.n2 == 1 && x.si == g.inner && y.si == g.inner &&
-           blocked_w() && lr->split_ok(c, x, y, g);
+    return !acc && c.dt == SMAT_C128 && g.n1 * g.n2 == 1 && lr->split_ok(c, x, y, g);
   }
-  static WhtArgs wht_args(const void* x, void* y) {
-    WhtArgs a;
-    a.x = x; a.y = y;
-    return a;
+  // row maps of the wlr passes (see wlr.cuh); lg(v) = log2 of a power of two
+  static int32_t lg(int64_t v) { return ilog2(v); }
+  // user rows (unit row = logical row): group T = g / NWa holds rows NWa T + a
+  WlrRows user_rows(int64_t ld) const {
+    WlrRows m;
+    m.g_lo = NWa; m.a_lo = 1; m.ld = ld;
+    return m;
   }
-  // pass A: 2^a-point transform over n1 (user rows r = n1 + N1*k2 <-> blocked)
-  void pass_a(Ctx& c, const void* x, void* y, bool to_blocked, int64_t K, int64_t n) const {
-    WhtArgs a = wht_args(x, y);
-    a.n2 = N2b; a.inner = K; a.nb = N2b * K;
-    const int64_t blk_lo = K, blk_hi = N2b * 64 * K;
-    // (the row split applies to both sides: the natural side's high stride is 64 rows)
-    if (to_blocked) {  // natural in, blocked out (forward)
-      a.xs2 = N1 * K; a.xsi = K; a.xsi_hi = 64 * K;
-      a.ys2 = 64 * K; a.ysi = blk_lo; a.ysi_hi = blk_hi;
-      a.n_valid_in = n;   // rows >= n are the zero padding
-    } else {           // blocked in, natural out (backward)
-      a.xs2 = 64 * K; a.xsi = blk_lo; a.xsi_hi = blk_hi;
-      a.ys2 = N1 * K; a.ysi = K; a.ysi_hi = 64 * K;
-      a.n_valid_out = n;  // rows >= n are truncated
-    }
-    a.i_lo_bits = 6;
-    a.g_div = K; a.g_mod = N2b; a.g_mul = N1; a.gin_stride = 1; a.gout_stride = 1;
-    c.wht(c.dt, int(N1), a);
+  WlrIn user_in(const void* p, int64_t ld, int64_t n) const {
+    WlrIn w;
+    w.kind = WLR_IN_ROWS; w.p = p; w.ld = ld; w.rows = n;
+    return w;
+  }
+  // T1 as written by A1 (groups T = b + 64 k2 of NWa rows a): row (k2 NWa + a) 64 + b
+  WlrRows t1_by_a(int64_t K) const {
+    WlrRows m;
+    m.gsh = 6; m.g_hi = 64 * NWa; m.g_lo = 1; m.a_lo = 64; m.ld = K;
+    return m;
+  }
+  WlrIn t1_by_a_in(const void* p, int64_t K) const {
+    WlrIn w;
+    w.kind = WLR_IN_T1A; w.p = p; w.ld = K; w.nwa = NWa; w.n2b = N2b; w.P = P;
+    return w;
+  }
+  // T1 as read by A2 (groups T' = k2 NWa + a of 64 rows b): row 64 T' + b
+  WlrRows t1_by_b(int64_t K) const {
+    WlrRows m;
+    m.g_lo = 64; m.a_lo = 1; m.ld = K;
+    return m;
+  }
+  WlrIn t1_by_b_in(const void* p, int64_t K) const {
+    WlrIn w;
+    w.kind = WLR_IN_ROWS; w.p = p; w.ld = K; w.rows = P;
+    return w;
+  }
+  // blocked T2 (groups T' = k2 NWa + a, rows b): n1 = a + NWa b ->
+  // ((n1 / 64) N2b + k2) 64 + n1 % 64, b = b_lo + (64 / NWa) b_hi
+  WlrRows t2_blocked(int64_t K) const {
+    WlrRows m;
+    m.gsh = lg(NWa); m.g_hi = 64; m.g_lo = 1;
+    m.ash = lg(64 / NWa); m.a_lo = NWa; m.a_hi = N2b * 64; m.ld = K;
+    return m;
+  }
+  WlrIn t2_blocked_in(const void* p, int64_t K) const {
+    WlrIn w;
+    w.kind = WLR_IN_T2B; w.p = p; w.ld = K; w.nwa = NWa; w.n2b = N2b; w.P = P;
+    return w;
   }
   // pass B: N2b-point transform over k2, blocked on both sides
   void pass_b(Ctx& c, const void* x, void* y, bool mask_in, int64_t K, int64_t n) const {
-    WhtArgs a = wht_args(x, y);
+    WhtArgs a;
+    a.x = x; a.y = y;
     a.xs1 = a.ys1 = N2b * 64 * K; a.xs2 = a.ys2 = K; a.xsi = a.ysi = 64 * K;
     a.n2 = 64; a.inner = K; a.nb = N1 * K;
     a.g_div = K; a.g_mod = N1; a.g_mul = 1; a.gin_stride = a.gout_stride = N1;
@@ -1146,42 +1202,61 @@ struct DFSumNode : Node {
       c.release(m0);
       return;
     }
-    const int64_t K = g.inner, n = rows;
+    const int64_t K = g.inner, n = rows, r = lr->r;
     Geo gb;
     gb.inner = K;
-    Blk Tb = c.alloc_blk(c.dt, gb, P);   // blocked
-    Blk Tmp = c.alloc_blk(c.dt, gb, P);  // blocked
+    Blk Ta = c.alloc_blk(c.dt, gb, P);
+    Blk Tb = c.alloc_blk(c.dt, gb, P);
     void* w = c.alloc(lr->w_bytes(c, g));
-    const bool fork = c.can_fork();
+    double* w3 = LowRankNode::w3_of(c, w, K);
+    const void* sv = lr->s ? lr->s->p : nullptr;
+    WlrMode ma, mb;
+    ma.nw = int(NWa); mb.nw = 64;
+    WlrArgs a1, a2;
+    a1.r = a2.r = r; a1.K = a2.K = K;
     if (!adj) {
       // y = DF (H_pad x + U diag(s) V^H x)
-      Ctx side = c;
-      if (fork) side.stream = c.fork();
-      side.launches = 0;
-      lr->contract(side, false, x, g, w);
-      c.launches += side.launches;
-      pass_a(c, x.p, Tmp.p, true, K, n);
-      pass_b(c, Tmp.p, Tb.p, false, K, n);
-      if (fork) c.join(side.stream);
-      lr->expand(c, false, w, Tb, g, true, N1, N2b);
-      XformIO io = df_io(false, Tb, y, n);
+      ma.con = true;  // A1: x -> T1 (Ta), partials of V^H x
+      a1.in = user_in(x.p, x.si, n);
+      a1.y = Ta.p; a1.yout = t1_by_a(K);
+      a1.F = lr->Vc->p; a1.n_f = n;
+      a1.nrows = P; a1.n_out = P;
+      a1.partial = w;
+      c.wlr(ma, a1, "wht_lowrank_a");
+      c.wlr_fin(w, r, K, sv, false, w3);
+      mb.exp = true;  // A2: T1 (Ta) -> T2 (Tb), + U~ W'
+      a2.in = t1_by_b_in(Ta.p, K);
+      a2.y = Tb.p; a2.yout = t2_blocked(K);
+      a2.F = lr->Ute->p; a2.n_f = P;
+      a2.nrows = P; a2.n_out = P;
+      a2.w3 = w3;
+      c.wlr(mb, a2, "wht_lowrank_b");
+      pass_b(c, Tb.p, Ta.p, false, K, n);
+      XformIO io = df_io(false, Ta, y, n);
       io.x_blk = true;
       run_xform(c, M, g, io);
     } else {
       // y = (H_pad + V diag(conj s) U^H) DF^H x
-      XformIO io = df_io(true, x, Tb, n);
+      XformIO io = df_io(true, x, Ta, n);
       io.y_blk = true;
-      io.y_rows = P;  // rows n..P come out zero (zero-padded post vector): finite for the P-row contraction
+      io.y_rows = P;  // rows n..P come out zero (zero-padded post vector)
       run_xform(c, M, g, io);
-      Ctx side = c;
-      if (fork) side.stream = c.fork();
-      side.launches = 0;
-      lr->contract(side, true, Tb, g, w, N1, N2b);
-      c.launches += side.launches;
-      pass_b(c, Tb.p, Tmp.p, true, K, n);
-      pass_a(c, Tmp.p, y.p, false, K, n);
-      if (fork) c.join(side.stream);
-      lr->expand(c, true, w, y, g, true);
+      pass_b(c, Ta.p, Tb.p, true, K, n);
+      mb.con = true;  // A2: T2 (Tb) -> T1 (Ta), partials of U~^H T2
+      a2.in = t2_blocked_in(Tb.p, K);
+      a2.y = Ta.p; a2.yout = t1_by_b(K);
+      a2.F = lr->Utc->p; a2.n_f = P;
+      a2.nrows = P; a2.n_out = P;
+      a2.partial = w;
+      c.wlr(mb, a2, "wht_lowrank_b");
+      c.wlr_fin(w, r, K, sv, true, w3);
+      ma.exp = true;  // A1: T1 (Ta) -> x', + V W''
+      a1.in = t1_by_a_in(Ta.p, K);
+      a1.y = y.p; a1.yout = user_rows(y.si);
+      a1.F = lr->Ve->p; a1.n_f = n;
+      a1.nrows = std::min(P, (n + 63) / 64 * 64); a1.n_out = n;
+      a1.w3 = w3;
+      c.wlr(ma, a1, "wht_lowrank_a");
     }
     c.release(m0);
   }
@@ -1656,24 +1731,57 @@ struct Builder {
     fourstep_split(M, N1, N2);
     const int64_t P = int64_t(1) << hp->had_order;
     if (N1 < 128 || N1 > kTileMax || P % N1 || P < n || hp->rows != n || hp->cols != n) return nullptr;
-    const int64_t N2b = P / N1;
-    if (N2b < 2 || N2b > N2 || N2b > kTileMax) return nullptr;
+    const int64_t N2b = P / N1, NWa = N1 / 64;
+    if (N2b < 2 || N2b > N2 || N2b > kTileMax || NWa < 2 || NWa > 64) return nullptr;
     auto* b = add<DFSumNode>();
     b->fallback = prod;
     b->df = df; b->hp = hp; b->lr = lr;
-    b->N1 = N1; b->N2 = N2; b->N2b = N2b; b->P = P; b->M = M;
-    if (lr->blas) {
-      lr->Ub = new_buf(p, SMAT_C128, P * lr->r);
-      block_rows_kernel<<<1184, 256>>>((const double2*)lr->U->p, (double2*)lr->Ub->p, n, lr->r, N1, N2b);
-      lr->Ubs = lr->Ub;
-      if (lr->s) {
-        lr->Ubs = new_buf(p, SMAT_C128, P * lr->r);
-        block_rows_kernel<<<1184, 256>>>((const double2*)lr->Us->p, (double2*)lr->Ubs->p, n, lr->r, N1, N2b);
-      }
-      SMAT_CUDA(cudaGetLastError());
-    }
-    p.fused = "blocked Bluestein/Hadamard/LowRank chain (N1=" + std::to_string(N1) + ", N2b=" + std::to_string(N2b) + ")";
+    b->N1 = N1; b->N2 = N2; b->N2b = N2b; b->P = P; b->M = M; b->NWa = NWa;
+    build_utilde(lr, n, N1, N2b, NWa);
+    p.fused = "blocked Bluestein/Hadamard/LowRank chain (N1=" + std::to_string(N1) + ", N2b=" + std::to_string(N2b) +
+              ", Hadamard " + std::to_string(NWa) + " x 64 x " + std::to_string(N2b) + ")";
     return b;
+  }
+
+  // U~ = H_{N2b} U / N2b over k2 (U zero-padded to P rows; logical row
+  // r = a + NWa b + N1 k2), stored in the blocked chain's A2 unit order:
+  // unit row (k2 NWa + a) 64 + b
+  DevBuf* build_utilde(LowRankNode* lr, int64_t n, int64_t N1, int64_t N2b, int64_t NWa) {
+    const int64_t P = N1 * N2b, r = lr->r;
+    DevBuf* Upad = new_buf(p, SMAT_C128, P * r);
+    SMAT_CUDA(cudaMemset(Upad->p, 0, Upad->bytes));
+    SMAT_CUDA(cudaMemcpy(Upad->p, lr->U->p, size_t(n * r) * 16, cudaMemcpyDeviceToDevice));
+    DevBuf* Uw = new_buf(p, SMAT_C128, P * r);
+    {
+      // N2b-point FWHT over k2 for every (n1, q): rows k2 N1 r elements apart
+      Ctx c;
+      c.device = p.device;
+      c.dt = SMAT_C128;
+      WhtArgs a;
+      a.x = Upad->p; a.y = Uw->p;
+      a.xs1 = a.ys1 = P * r; a.xs2 = a.ys2 = r; a.xsi = a.ysi = N1 * r;
+      a.n2 = N1; a.inner = r; a.nb = N1 * r;
+      c.wht(SMAT_C128, int(N2b), a);
+    }
+    DevBuf* Ut = new_buf(p, SMAT_C128, P * r);
+    utilde_perm_kernel<<<1184, 256>>>((const double2*)Uw->p, (double2*)Ut->p, P, r, N1, NWa, 1.0 / double(N2b));
+    SMAT_CUDA(cudaGetLastError());
+    lr->Utc = new_buf(p, SMAT_C128, P * wlr_pitch(false));
+    lr->Ute = new_buf(p, SMAT_C128, P * wlr_pitch(true));
+    wlr_pad_factor(Ut->p, lr->Utc->p, P, r, false, nullptr);
+    wlr_pad_factor(Ut->p, lr->Ute->p, P, r, true, nullptr);
+    SMAT_CUDA(cudaDeviceSynchronize());
+    drop_buf(Upad);
+    drop_buf(Uw);
+    drop_buf(Ut);
+    return nullptr;
+  }
+  void drop_buf(DevBuf* b) {
+    for (auto it = p.bufs.begin(); it != p.bufs.end(); ++it)
+      if (it->get() == b) {
+        p.bufs.erase(it);
+        return;
+      }
   }
 
   std::vector<Node*> memo;  // shared sub-operators are compiled once
@@ -1711,29 +1819,16 @@ struct Builder {
         n->U = upload_param(p, nd.param[0], p.dt);
         n->V = upload_param(p, nd.param[1], p.dt);
         if (nd.param[2].len) n->s = upload_param(p, nd.param[2], p.dt);
-        if (dt_complex(p.dt) && blas_available() && n->r <= 32) {
-          n->blas = true;
-          blas_warm(p.device);
-          n->Us = n->U;
-          n->Vs = n->V;
-          if (n->s) {
-            // U diag(s), V diag(conj s) formed in fp64 on the host, stored at
-            // the plan precision
-            auto scaled = [&](const smat_param& f, int64_t nrows, bool cj) {
-              auto hf = convert_host(f, SMAT_C128);
-              auto hs = convert_host(nd.param[2], SMAT_C128);
-              const std::complex<double>* fv = (const std::complex<double>*)hf.data();
-              const std::complex<double>* sv = (const std::complex<double>*)hs.data();
-              std::vector<std::complex<double>> o(size_t(nrows * n->r));
-              for (int64_t i = 0; i < nrows; ++i)
-                for (int64_t q = 0; q < n->r; ++q)
-                  o[size_t(i * n->r + q)] = fv[i * n->r + q] * (cj ? std::conj(sv[q]) : sv[q]);
-              smat_param prm{o.data(), nrows * n->r, SMAT_C128, 0};
-              return upload_param(p, prm, p.dt);
-            };
-            n->Us = scaled(nd.param[0], nd.rows, false);
-            n->Vs = scaled(nd.param[1], nd.cols, true);
-          }
+        if (p.dt == SMAT_C128 && n->r <= 32) {
+          auto padded = [&](DevBuf* f, int64_t nrows, bool e) {
+            DevBuf* b = new_buf(p, SMAT_C128, nrows * wlr_pitch(e));
+            wlr_pad_factor(f->p, b->p, nrows, n->r, e, nullptr);
+            return b;
+          };
+          n->Uc = padded(n->U, nd.rows, false);
+          n->Ue = padded(n->U, nd.rows, true);
+          n->Vc = padded(n->V, nd.cols, false);
+          n->Ve = padded(n->V, nd.cols, true);
         }
         out = n;
         break;
@@ -2026,23 +2121,100 @@ Plan* build_plan(const smat_node* nodes, int n_nodes, const int32_t* children, i
   return p.release();
 }
 
-void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, void* y, int64_t ncols) {
+static void run_root(const Plan& p, Ctx& c, bool adj, Blk xb, const Blk& yb, const Geo& g, int64_t nin) {
+  if (xb.dt != p.dt && !p.root->accepts_real()) xb = promote(c, xb, g, nin);
+  p.root->apply(c, adj, xb, yb, g, false);
+}
+
+// Row-major view of a (rows, ncols) block with leading dimension ld.
+static Blk row_view(const void* ptr, int dt, int64_t ld, int64_t rows) {
+  Blk b;
+  b.p = const_cast<void*>(ptr);
+  b.dt = dt;
+  b.si = ld;
+  b.s2 = b.s1 = rows * ld;
+  return b;
+}
+
+// Copy between a user block (row-major with leading dimension ld, or
+// column-major) and a dense row-major block: one pointwise launch.
+static void stage_copy(Ctx& c, int dt, const void* src, void* dst, int64_t rows, int64_t ncols, int64_t ld,
+                       int layout, bool to_dense) {
+  PointArgs pa;
+  pa.x = src; pa.x_dt = dt; pa.y = dst; pa.y_dt = dt;
+  int64_t us2, usi, uinner_stride;
+  if (layout == SMAT_COL_MAJOR) {
+    // element (i, col) at col*ld + i: batches o2 = col (stride ld), rows stride 1
+    pa.n2 = ncols; pa.inner = 1; pa.nb = ncols; pa.n = rows;
+    us2 = ld; usi = 1; uinner_stride = 0;
+    const int64_t ds2 = 1, dsi = ncols;
+    if (to_dense) { pa.xs2 = us2; pa.xsi = usi; pa.ys2 = ds2; pa.ysi = dsi; }
+    else { pa.xs2 = ds2; pa.xsi = dsi; pa.ys2 = us2; pa.ysi = usi; }
+  } else {
+    pa.n2 = 1; pa.inner = ncols; pa.nb = ncols; pa.n = rows;
+    us2 = rows * ld; usi = ld; uinner_stride = 1;
+    if (to_dense) { pa.xs2 = us2; pa.xsi = usi; pa.ys2 = rows * ncols; pa.ysi = ncols; }
+    else { pa.xs2 = rows * ncols; pa.xsi = ncols; pa.ys2 = us2; pa.ysi = usi; }
+  }
+  (void)uinner_stride;
+  pa.xs1 = pa.xs2 * pa.n2;
+  pa.ys1 = pa.ys2 * pa.n2;
+  c.point_dt(dt, pa);
+}
+
+void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, int64_t ldx, void* y, int64_t ldy,
+              int64_t ncols, int layout) {
   const bool adj = dir == 1;
   const int64_t nin = adj ? p.rows : p.cols, nout = adj ? p.cols : p.rows;
+  const bool col = layout == SMAT_COL_MAJOR;
+  SMAT_CHECK(layout == SMAT_ROW_MAJOR || col, SMAT_BAD_ARG, "layout must be SMAT_ROW_MAJOR or SMAT_COL_MAJOR");
+  if (ldx <= 0) ldx = col ? nin : ncols;
+  if (ldy <= 0) ldy = col ? nout : ncols;
+  SMAT_CHECK(ldx >= (col ? nin : ncols) && ldy >= (col ? nout : ncols), SMAT_BAD_ARG,
+             "leading dimension smaller than the block");
   Geo g;
   g.inner = ncols;
-  Blk xb;
-  xb.p = (void*)x;
-  xb.dt = x_dt;
-  xb.si = ncols;
-  xb.s2 = xb.s1 = nin * ncols;
-  Blk yb;
-  yb.p = y;
-  yb.dt = p.dt;
-  yb.si = ncols;
-  yb.s2 = yb.s1 = nout * ncols;
-  if (x_dt != p.dt && !p.root->accepts_real()) xb = promote(c, xb, g, nin);
-  p.root->apply(c, adj, xb, yb, g, false);
+  if (!col) {
+    const Blk xb = row_view(x, x_dt, ldx, nin), yb = row_view(y, p.dt, ldy, nout);
+    if (ldx == ncols && ldy == ncols) {
+      run_root(p, c, adj, xb, yb, g, nin);
+      return;
+    }
+    // strided rows in place when every pass of the plan can address them
+    // (a host-side dry run of the plan decides; no launch happens in it)
+    Ctx d = c;
+    d.measure = true;
+    d.prof = nullptr;
+    d.launches = 0;
+    bool direct = true;
+    try {
+      run_root(p, d, adj, xb, yb, g, nin);
+    } catch (const Error& e) {
+      if (e.code != SMAT_UNSUPPORTED) throw;
+      direct = false;
+    }
+    if (direct) {
+      if (c.measure) {
+        c.peak = std::max(c.peak, d.peak);
+        c.launches += d.launches;
+      } else {
+        run_root(p, c, adj, xb, yb, g, nin);
+      }
+      return;
+    }
+  }
+  // staged: dense row-major copies of the strided / column-major sides
+  const size_t m0 = c.mark();
+  const bool sx = col || ldx != ncols, sy = col || ldy != ncols;
+  Blk xb = row_view(x, x_dt, ncols, nin), yb = row_view(y, p.dt, ncols, nout);
+  if (sx) {
+    xb = c.alloc_blk(x_dt, g, nin);
+    stage_copy(c, x_dt, x, xb.p, nin, ncols, ldx, layout, true);
+  }
+  if (sy) yb = c.alloc_blk(p.dt, g, nout);
+  run_root(p, c, adj, xb, yb, g, nin);
+  if (sy) stage_copy(c, p.dt, yb.p, y, nout, ncols, ldy, layout, false);
+  c.release(m0);
 }
 
 }  // namespace smat

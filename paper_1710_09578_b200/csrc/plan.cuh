@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "misc_kernels.cuh"
 #include "tile_kernels.cuh"
+#include "wlr.cuh"
 
 namespace smat {
 
@@ -107,6 +108,12 @@ struct Ctx {
     note("point");
     if (!measure) launch_point(dt, a, stream);
   }
+  // pointwise pass in an explicit dtype (staging copies of the apply's user blocks)
+  void point_dt(int pdt, const PointArgs& a) {
+    ++launches;
+    note("stage");
+    if (!measure) launch_point(pdt, a, stream);
+  }
   void gather(const IndexArgs& a) {
     ++launches;
     note("gather");
@@ -137,6 +144,18 @@ struct Ctx {
                  int64_t ldb, double beta, void* C, int64_t ldc) {
     note("gemm_blas");
     if (!measure) blas_gemm(dt, device, stream, opa, opb, m, n, k, A, lda, B, ldb, beta, C, ldc);
+  }
+  // fused Hadamard + LowRank pass / plain LowRank half on FP64 tensor cores (wlr.cu)
+  void wlr(const WlrMode& m, const WlrArgs& a, const char* label) {
+    launches += launch_wlr(m, a, device, stream, true);
+    note(label);
+    if (!measure) launch_wlr(m, a, device, stream, false);
+  }
+  void wlr_fin(const void* partial, int64_t r, int64_t K, const void* s, bool s_conj, double* w3) {
+    const int grid = wlr_grid(device, K);
+    launches += launch_wlr_finalize(partial, grid, r, K, s, s_conj, w3, stream, true);
+    note("lowrank_finalize");
+    if (!measure) launch_wlr_finalize(partial, grid, r, K, s, s_conj, w3, stream, false);
   }
   void lr_contract(const LowRankArgs& a) {
     launches += launch_lowrank_contract(dt, a, device, stream, true);
@@ -197,7 +216,10 @@ struct Plan {
 // builders (plan.cu)
 Plan* build_plan(const smat_node* nodes, int n_nodes, const int32_t* children, int n_children,
                  int root, int dt, int device);
-void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, void* y, int64_t ncols);
+// y = A x (dir 0) or A^H x (dir 1); x / y row-major with leading dimensions
+// ldx / ldy (0: dense) or column-major (layout SMAT_COL_MAJOR)
+void run_plan(const Plan& p, Ctx& c, int dir, const void* x, int x_dt, int64_t ldx, void* y, int64_t ldy,
+              int64_t ncols, int layout);
 
 // helpers shared with fused.cu
 DevBuf* upload_param(Plan& p, const smat_param& prm, int target_dt);

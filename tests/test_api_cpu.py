@@ -26,7 +26,21 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(_native.LIB_PATH))
     for name in declared:
         assert hasattr(lib, name), name
-    assert _native.load_library().smat_abi_version() == 2
+    assert _native.load_library().smat_abi_version() == 3
+
+
+def test_block_layout_classification():
+    """Strided views reach the engine with their leading dimension (no copy):
+    column slices of a wider row-major block, and column-major blocks."""
+    from paper_1710_09578_b200.core import _block_layout
+
+    assert _block_layout(8, 1, 100, 8) == (0, _native.ROW_MAJOR)          # dense
+    assert _block_layout(64, 1, 100, 8) == (64, _native.ROW_MAJOR)        # column slice
+    assert _block_layout(64, 0, 100, 1) == (64, _native.ROW_MAJOR)        # one column of a block
+    assert _block_layout(1, 100, 100, 8) == (100, _native.COL_MAJOR)      # Fortran order
+    assert _block_layout(1, 128, 100, 8) == (128, _native.COL_MAJOR)      # slice of a Fortran block
+    assert _block_layout(2, 3, 100, 8)[0] == -1                           # neither: dense copy
+    assert _block_layout(-8, 1, 100, 8)[0] == -1                          # negative stride
 
 
 def test_struct_layout_matches_header():

@@ -483,3 +483,81 @@ def test_c5_chain_random_sizes():
         _close(by, orc.apply(oo, Y, 1), 1e-12, f"C5-type bwd N={N} K={K} r={r}")
         lhs, rhs = np.vdot(Y, fx), np.vdot(by, X)
         assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(X) * np.linalg.norm(Y) * np.sqrt(N)
+
+
+# ------------------------------------------------ strided views (ABI v3) ----
+def _c5_small(N, seed):
+    rng = np.random.default_rng(seed)
+    d1 = np.exp(2j * np.pi * rng.random(N))
+    d2 = np.exp(2j * np.pi * rng.random(N))
+    U = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    V = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    idx = np.arange(N)
+    order = (N - 1).bit_length()
+    op = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2),
+                    sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx), sm.LowRank(U, V)))
+    return op, orc.chain_c5(N, d1, d2, U, V), rng
+
+
+def test_strided_column_slices_in_place():
+    """A column slice of a wider row-major block (leading dimension > ncols)
+    goes through smat_apply with its leading dimension: no staging copy (the
+    workspace is the dense one) and the same result as the dense block — for
+    the four-step convolution (C2 path) and the blocked C5 chain."""
+    import torch
+
+    from paper_1710_09578_b200 import _native
+
+    rng = np.random.default_rng(77)
+    n = 1 << 16
+    c = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    big = torch.from_numpy(rng.standard_normal((n, 16)) + 1j * rng.standard_normal((n, 16))).cuda()
+    view = big[:, 3:9]
+    assert not view.is_contiguous()
+    op = sm.Circulant(c)
+    plan = op.plan_for(np.complex128)
+    for d in (0, 1):
+        assert plan.workspace_bytes(d, 6, 16, 0, _native.ROW_MAJOR) == plan.workspace_bytes(d, 6)
+    oc = orc.circulant(c)
+    xs = view.cpu().numpy()
+    _close(op.forward(view).cpu().numpy(), orc.apply(oc, xs, 0), 1e-12, "strided circulant fwd")
+    _close(op.backward(view).cpu().numpy(), orc.apply(oc, xs, 1), 1e-12, "strided circulant bwd")
+
+    N = 70001
+    op5, o5, rng = _c5_small(N, 5)
+    big = torch.from_numpy(rng.standard_normal((N, 12)) + 1j * rng.standard_normal((N, 12))).cuda()
+    view = big[:, 5:12]
+    plan = op5.plan_for(np.complex128)
+    for d in (0, 1):
+        assert plan.workspace_bytes(d, 7, 12, 0, _native.ROW_MAJOR) == plan.workspace_bytes(d, 7)
+    xs = view.cpu().numpy()
+    _close(op5.forward(view).cpu().numpy(), orc.apply(o5, xs, 0), 1e-12, "strided C5 fwd")
+    _close(op5.backward(view).cpu().numpy(), orc.apply(o5, xs, 1), 1e-12, "strided C5 bwd")
+
+
+def test_column_major_and_staged_views():
+    """Column-major blocks (a transposed tensor) and strided views that a
+    plan cannot address in place are staged through the workspace with one
+    device copy each way; numpy strided arrays take pitched host copies."""
+    import torch
+
+    rng = np.random.default_rng(78)
+    n, K = 1 << 14, 5
+    xt = torch.from_numpy(rng.standard_normal((K, n)) + 1j * rng.standard_normal((K, n))).cuda()
+    x = xt.t()  # (n, K) column-major view
+    for op, oo in ((sm.Hadamard(14), orc.hadamard(14)), (sm.Fourier(n), orc.fourier(n)),
+                   (sm.Kron(sm.Hadamard(4), sm.Fourier(1 << 10)), orc.kron(orc.hadamard(4), orc.fourier(1 << 10)))):
+        xs = x.cpu().numpy()
+        _close(op.forward(x).cpu().numpy(), orc.apply(oo, xs, 0), 1e-12, f"col-major {op!r} fwd")
+        _close(op.backward(x).cpu().numpy(), orc.apply(oo, xs, 1), 1e-12, f"col-major {op!r} bwd")
+        wide = x.contiguous()
+        big = torch.zeros((n, 2 * K), dtype=wide.dtype, device="cuda")
+        big[:, 1:1 + K] = wide
+        sl = big[:, 1:1 + K]
+        _close(op.forward(sl).cpu().numpy(), orc.apply(oo, xs, 0), 1e-12, f"slice {op!r} fwd")
+    # numpy host arrays: a column slice and a Fortran-order block
+    A = rng.standard_normal((n, 9))
+    oo = orc.hadamard(14)
+    _close(sm.Hadamard(14).forward(A[:, 2:7]), orc.apply(oo, A[:, 2:7], 0), 0, "numpy slice")
+    F = np.asfortranarray(A)
+    _close(sm.Hadamard(14).forward(F), orc.apply(oo, A, 0), 0, "numpy fortran")
