@@ -60,13 +60,17 @@ constexpr int DP = KCB * 16;        // 1056
 constexpr int FPC = (RK + 2) * 16;  // 544, contraction
 constexpr int FPE = (RK + 4) * 16;  // 576, expansion
 constexpr int NTHR = 256;
+// ring depth per CTA and CTAs per SM: one single-stage CTA per ~half SM, so
+// that while one CTA waits for its tile or stores, the other multiplies
+constexpr int NST = 1;
+constexpr int MINB = 2;
 
 template <bool EXP>
 struct WlrGeom {
   static constexpr int FP = EXP ? FPE : FPC;
   static constexpr int DATA = TR * DP;
   static constexpr int STAGE = DATA + TR * FP;
-  static constexpr int SMEM = 2 * STAGE + 64;
+  static constexpr int SMEM = NST * STAGE + 64;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -139,12 +143,12 @@ __device__ __forceinline__ void wht_stage(unsigned char* dbuf, int c, int p) {
 }
 
 template <int NW, bool CON, bool EXP, bool IN, bool OUT>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(NTHR, MINB)
     wlr_kernel(const __grid_constant__ CUtensorMap xmap, const WlrArgs a, const int nchunks, const int nunits) {
   using G = WlrGeom<EXP>;
   constexpr int FP = G::FP;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * G::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * G::STAGE);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ch = int(blockIdx.x) % nchunks;
   const int64_t c0 = int64_t(ch) * KC;
@@ -185,11 +189,10 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (tid == 0) {
     if constexpr (IN) tma_prefetch_desc(&xmap);
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int st = 0; st < NST; ++st) mbar_init(&bars[st], 1);
     fence_barrier_init();
-    if (int(blockIdx.x) < nunits) issue(blockIdx.x, 0);
-    if (int(blockIdx.x) + gs < nunits) issue(blockIdx.x + gs, 1);
+    for (int st = 0; st < NST; ++st)
+      if (int(blockIdx.x) + st * gs < nunits) issue(blockIdx.x + st * gs, st);
   }
   __syncthreads();
 
@@ -214,11 +217,11 @@ __global__ void __launch_bounds__(NTHR, 1)
   }
 
   for (int u = blockIdx.x, it = 0; u < nunits; u += gs, ++it) {
-    const int s = it & 1;
+    const int s = it % NST;
     unsigned char* dbuf = smem + s * G::STAGE;
     unsigned char* fbuf = dbuf + G::DATA;
     const int64_t g0 = int64_t(u / nchunks) * TR;
-    mbar_wait(&bars[s], uint32_t((it >> 1) & 1));
+    mbar_wait(&bars[s], uint32_t((it / NST) & 1));
     // zero what the copies did not fill: the whole tile without an input,
     // factor rows past the factor's end
     const int rf = rows_valid(min(a.n_f, a.nrows), g0);
@@ -303,9 +306,9 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
     __syncthreads();  // stage s is free
-    if (tid == 0 && u + 2 * gs < nunits) {
+    if (tid == 0 && u + NST * gs < nunits) {
       fence_proxy_async();
-      issue(u + 2 * gs, s);
+      issue(u + NST * gs, s);
     }
   }
 
@@ -423,7 +426,7 @@ void wlr_pad_factor(const void* src, void* dst, int64_t rows, int64_t r, bool ex
 
 int wlr_grid(int device, int64_t K) {
   const int nchunks = int((K + KC - 1) / KC);
-  const int per = num_sms(device) / nchunks;
+  const int per = MINB * num_sms(device) / nchunks;
   return nchunks * (per > 0 ? per : 1);
 }
 
