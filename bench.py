@@ -1,35 +1,44 @@
 """Benchmark of the structured-transform hot path on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl reference]
 
-Metric: forward/backward column throughput of one transform (columns/s) —
-one step = forward A·X then backward A^H·Y over the whole (rows, K) block of
-the workload, so value = 2K / step time (column-transforms per second, both
-directions counted).  Default workload: BASELINE config C2 (Circulant 2^20,
-64 complex64 columns) = configs[1]; c1..c5 select the others.
+Metric (BASELINE.json): forward/backward column throughput of one transform
+(columns/s) — one step = forward A·X then backward A^H·Y over the whole
+(rows, K) block of the workload, value = 2K / step time, with the achieved
+HBM GB/s and roofline fractions beside it.  Default workload: C5, the largest
+single-GPU configuration and the one at the reference's own arithmetic width
+(Diag·Fourier(1,000,003)·Diag·Sum(Hpad, LowRank32), 1,000,003 x 128
+complex128); c1..c4 select the other BASELINE configs, whose device numbers
+also appear under `per_config` of the default line.
 
-Device timing: inputs resident in HBM, W untimed warm-up steps, then exactly
-K steps bracketed by barrier + cuda.synchronize, CUDA events on the launching
-stream, max over ranks.  Working sets exceed the 126 MB L2 for c2..c5; c1 is
-L2-flushed between steps (a 256 MB write).  Multi-GPU (torchrun): one process
-per GPU, every rank transforms its own full K-column block (weak scaling,
-column sharding, no collective on the data path; NCCL only for the barrier and
-the max-over-ranks timing reduction).
+Multi-GPU: the named block is split into contiguous column
+slices, one per GPU (strong scaling, no collective on the data path).
+`--gpus N` without a torchrun environment launches the N ranks itself
+(torch.distributed.run, 127.0.0.1); NCCL carries only the barrier and the
+max-over-ranks timing reduction.  value = 2K / max-over-ranks step time.
 
-Extra keys: e2e (the same metric through the public API with pinned HOST
-buffers, H2D+D2H inside the timed region), roofline (dominant kernel,
-algorithmic bytes per launch / its CUDA-event duration vs MEASURED_PEAKS.json),
-cpu_baseline (the CPU oracle — a numpy port of the reference algorithm — on a
-bounded sample on the host), gpu_launches, clocks.
+Device timing: inputs resident in HBM, W untimed warm-up steps, every rank's
+step captured in one CUDA graph and replayed; exactly K steps bracketed by
+barrier + cuda.synchronize, CUDA events on the launching stream.  Working
+sets exceed the 126 MB L2 for c2..c5; c1 is L2-flushed between steps.
 
---impl reference: times the reference algorithm's CPU implementation (the
-oracle port; the reference is pure Python and cannot be installed on the GPU
-box) with all host cores (one process per column), rank 0 only.
+Parity gate: before printing, at least 8 columns (including the first and the
+last) of the timed step's outputs are compared with the CPU oracle (north
+star: relative L2 <= 1e-12 complex128 / float64, <= 1e-5 complex64 / float32,
+int32 and C1 float64 bit-exact).  A failing check prints no value and exits 1.
 
-SURVEY.md §8(f) rows, one JSON line each (not driver workloads):
-  --workload cg      device CG on C2's operator (normal equations, 64 rhs)
-  --workload ista    the reference bench's ISTA scenario at size 2^20
-  --workload sparse  Sparse (CSR) fwd + bwd, 2^20 x 2^20 with 16.8 M nonzeros
+Extra keys: roofline (dominant kernel: algorithmic bytes per launch / its
+CUDA-event duration vs MEASURED_PEAKS.json; step-level HBM fraction; FP64
+fraction vs the box's measured DFMA / DMMA peak), e2e (the same metric through
+op.forward / op.backward on pinned HOST buffers, copies inside the timed
+region), cpu_baseline (single-core oracle port on a bounded sample),
+gpu_launches, clocks, parity, per_config.
+
+--impl reference: the UNMODIFIED reference package (baseline/_ref/linopkit,
+installed with pip --no-deps from /root/reference) on the host cores, one
+process per sampled column, rank 0 only.
+
+--workload cg|ista|sparse: SURVEY.md §8(f) workloads (tools/bench_extra.py).
 """
 
 from __future__ import annotations
@@ -37,6 +46,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -49,18 +59,28 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "fwd/bwd columns/s and achieved HBM GB/s per transform vs B200 HBM peak"
 UNIT = "columns/s"
+NAMES = {1: "C1 Hadamard(10) 1024x16 float64", 2: "C2 Circulant(2^20) 2^20x64 complex64",
+         3: "C3 Toeplitz(3000x3000) 3000x4096 float32",
+         4: "C4 Kron(Hadamard(6),Fourier(128),Circulant(256)) 2^21x32 complex64",
+         5: "C5 Diag(d1)·Fourier(1000003)·Diag(d2)·Sum(Hpad,LowRank32) 1000003x128 complex128"}
+DTYPES = {1: "f64", 2: "c64", 3: "f32", 4: "c64", 5: "c128"}
+TOL = {1: 0.0, 2: 1e-5, 3: 1e-5, 4: 1e-5, 5: 1e-12}
+FULL_COLS = {1: 16, 2: 64, 3: 4096, 4: 32, 5: 128}
 
 
-def _args():
+def _args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "cg", "ista", "sparse"])
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "cg", "ista", "sparse"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--parity-cols", type=int, default=8)
+    return ap.parse_args(argv)
 
 
 def _dist_env():
@@ -70,18 +90,22 @@ def _dist_env():
     return rank, world, local
 
 
-def _workload_config(cfg: int):
-    from paper_1710_09578_b200 import configs
-
-    names = {1: "C1 Hadamard(10) 1024x16 float64", 2: "C2 Circulant(2^20) 2^20x64 complex64",
-             3: "C3 Toeplitz(3000x3000) 3000x4096 float32",
-             4: "C4 Kron(Hadamard(6),Fourier(128),Circulant(256)) 2^21x32 complex64",
-             5: "C5 Diag(d1)·Fourier(1000003)·Diag(d2)·Sum(Hpad,LowRank32) 1000003x128 complex128"}
-    dtypes = {1: "f64", 2: "c64", 3: "f32", 4: "c64", 5: "c128"}
-    return names[cfg], dtypes[cfg], configs
+def _log(*a):
+    print(*a, file=sys.stderr, flush=True)
 
 
-# --------------------------------------------------------------- CPU legs ----
+# ------------------------------------------------------------- launcher -----
+def _launch_ranks(args) -> int:
+    """--gpus N outside torchrun: start N ranks on this node ourselves."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# --------------------------------------------------------------- oracle -----
 def _oracle_op(cfg, w):
     from oracle import linop_oracle as orc
 
@@ -97,38 +121,90 @@ def _oracle_op(cfg, w):
     return orc.chain_c5(p["N"], p["d1"], p["d2"], p["U"], p["V"])
 
 
-# columns per CPU sample so one sample is ~10-30 s of single-core numpy work
-_SAMPLE_COLS = {1: 16, 2: 8, 3: 512, 4: 8, 5: 4}
-
-_POOL_STATE = {}
-
-
-def _pool_init(cfg):
-    from paper_1710_09578_b200 import configs
-
-    w = configs.make(cfg, ncols=1)
-    _POOL_STATE["w"] = w
-    _POOL_STATE["op"] = _oracle_op(cfg, w)
-    _POOL_STATE["cfg"] = cfg
+def parity_columns(K: int, want: int) -> list[int]:
+    """At least `want` global columns (all when K <= want), always including
+    the first and the last, the rest evenly spaced."""
+    if K <= want:
+        return list(range(K))
+    cols = {0, K - 1}
+    for c in np.linspace(0, K - 1, num=want).astype(int).tolist():
+        if len(cols) >= want:
+            break
+        cols.add(int(c))
+    return sorted(cols)
 
 
-def _pool_column(j):
+def rank_parity(cfg, w, a, b, want, fetch):
+    """This rank's share of the parity gate: the checked global columns inside
+    its slice [a, b), fetched (local indices -> (y, z) host arrays) and
+    compared with the oracle; None when it owns none of them."""
+    mine = [c for c in parity_columns(w.ncols, want) if a <= c < b]
+    if not mine:
+        return None
+    y, z = fetch([c - a for c in mine])
+    return check_parity(cfg, w, _oracle_op(cfg, w), np.ascontiguousarray(w.X[:, mine]), y, z, mine)
+
+
+def reduce_over_ranks(ms, par, cfg, world, device):
+    """Slowest rank's timed-region milliseconds and the combined parity report
+    (max errors over ranks; passes only if every rank's columns pass)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(ms)], device=device, dtype=torch.float64)
+    ok = torch.tensor([1 if (par is None or par["pass"]) else 0], device=device, dtype=torch.int32)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, par)
+        pars = [p for p in gathered if p]
+    else:
+        pars = [par] if par else []
+    parity = {"columns": sorted(c for p in pars for c in p["columns"]), "tol": TOL[cfg], "pass": bool(ok.item()),
+              "oracle": "oracle/linop_oracle.py (pinned to the reference's outputs, tests/golden)"}
+    for k in ("rel_l2_fwd", "rel_l2_bwd", "max_col_rel_l2_fwd", "max_col_rel_l2_bwd", "ref_metric_fwd",
+              "ref_metric_bwd"):
+        parity[k] = max((p[k] for p in pars), default=None)
+    return float(t.item()), parity
+
+
+def check_parity(cfg, w, oop, x_cols, y_cols, z_cols, cols):
+    """North-star metrics of the checked columns: relative L2 (block and max
+    per column) and the reference's max|err| / (1 + max|ref|)."""
     from oracle import linop_oracle as orc
 
-    w, op = _POOL_STATE["w"], _POOL_STATE["op"]
-    x = w.X[:, :1]
-    t0 = time.perf_counter()
-    y = orc.apply(op, x, 0)
-    orc.apply(op, y, 1)
-    return time.perf_counter() - t0
+    tol = TOL[cfg]
+    ry = orc.apply(oop, x_cols, 0)
+    rz = orc.apply(oop, ry, 1)
+    out = {"columns": [int(c) for c in cols], "tol": tol}
+    ok = True
+    for name, got, ref in (("fwd", y_cols, ry), ("bwd", z_cols, rz)):
+        got = np.asarray(got, dtype=np.complex128 if np.iscomplexobj(got) or np.iscomplexobj(ref) else np.float64)
+        num = np.linalg.norm(got - ref, axis=0)
+        den = np.linalg.norm(ref, axis=0)
+        den[den == 0] = 1.0
+        blk = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+        col = float(np.max(num / den))
+        refm = float(np.max(np.abs(got - ref)) / (1.0 + np.max(np.abs(ref))))
+        out[f"rel_l2_{name}"] = blk
+        out[f"max_col_rel_l2_{name}"] = col
+        out[f"ref_metric_{name}"] = refm
+        if tol == 0.0:
+            ok &= bool(np.array_equal(got, ref))
+        else:
+            ok &= blk <= tol and col <= tol
+    out["pass"] = bool(ok)
+    return out
 
 
-def cpu_baseline(cfg: int, cols: int | None = None):
+# --------------------------------------------------------------- CPU legs ---
+def cpu_baseline(cfg: int, cols: int = 4):
     """Single-core oracle (numpy port of the reference algorithm) on `cols` columns."""
     from oracle import linop_oracle as orc
     from paper_1710_09578_b200 import configs
 
-    cols = cols or _SAMPLE_COLS[cfg]
+    cols = min(cols, FULL_COLS[cfg]) if cfg != 3 else 512
     w = configs.make(cfg, ncols=cols)
     op = _oracle_op(cfg, w)
     orc.apply(op, w.X[:, :1], 0)  # warm the lru-cached plans (reference bench.py:263-270)
@@ -137,49 +213,108 @@ def cpu_baseline(cfg: int, cols: int | None = None):
     orc.apply(op, y, 1)
     dt = time.perf_counter() - t0
     return {"value": 2 * cols / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{cols} of {_full_cols(cfg)} columns, forward then backward, "
-                      f"numpy oracle single-threaded ({dt:.2f} s)"}
+            "sample": f"{cols} of {FULL_COLS[cfg]} columns, forward then backward, numpy port of the "
+                      f"reference algorithm (oracle/linop_oracle.py), single-threaded ({dt:.2f} s)"}
 
 
-def _full_cols(cfg):
-    return {1: 16, 2: 64, 3: 4096, 4: 32, 5: 128}[cfg]
+_REF = {}
+
+
+def _ref_module():
+    """The unmodified reference package: baseline/_ref (pip --target install of
+    /root/reference, travels with the repo), else /root/reference/pkg/src."""
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "linopkit" / "__init__.py").exists():
+            sys.path.insert(0, str(p))
+            try:
+                import linopkit  # noqa: F401
+
+                return linopkit, str(p)
+            except Exception as e:  # pragma: no cover - environment dependent
+                _log(f"reference import from {p} failed: {e}")
+            finally:
+                sys.path.remove(str(p))
+    return None, None
+
+
+def reference_op(lk, cfg, w):
+    """The config's operator through the reference's own public API (the
+    Sum / LowRank vehicle of SURVEY.md §8c for C5)."""
+    p = w.params
+    if cfg == 1:
+        return lk.Hadamard(p["order"])
+    if cfg == 2:
+        return lk.Circulant(p["c"])
+    if cfg == 3:
+        return lk.Toeplitz(p["col"], p["row_rest"])
+    if cfg == 4:
+        return lk.Kron(lk.Hadamard(p["h_order"]), lk.Fourier(p["f_n"]), lk.Circulant(p["c"]))
+    N = p["N"]
+    idx = np.arange(N)
+    hpad = lk.Partial(lk.Hadamard((N - 1).bit_length()), idx, idx)
+    lr = lk.Product(lk.Dense(p["U"]), lk.Dense(np.ascontiguousarray(p["V"].conj().T)))
+    s = lk.Product(lk.Blocks([[hpad, lr]]), lk.Blocks([[lk.Identity(N)], [lk.Identity(N)]]))
+    return lk.Product(lk.Diagonal(p["d1"]), lk.Fourier(N), lk.Diagonal(p["d2"]), s)
+
+
+def _ref_column(j):
+    op, X, apply = _REF["op"], _REF["X"], _REF["apply"]
+    x = np.ascontiguousarray(X[:, j % X.shape[1]])
+    t0 = time.perf_counter()
+    apply(op, apply(op, x, 0), 1)
+    return time.perf_counter() - t0
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference algorithm's CPU path with all host cores."""
+    """--impl reference: the reference's own CPU path with all host threads."""
     import multiprocessing as mp
 
     rank, world, _ = _dist_env()
     if rank != 0:
-        return
-    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    name, dtype, _ = _workload_config(cfg)
-    per_step = max(1, min(ncpu, _full_cols(cfg)))
-    ctx = mp.get_context("fork")
-    with ctx.Pool(per_step, initializer=_pool_init, initargs=(cfg,)) as pool:
-        pool.map(_pool_column, range(per_step))  # warm-up: plans + page-in
-        for _ in range(max(0, args.warmup - 1)):
-            pool.map(_pool_column, range(per_step))
+        return 0
+    from paper_1710_09578_b200 import configs
+
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    per_step = max(1, min(ncpu, FULL_COLS[cfg]))
+    lk, where = _ref_module()
+    w = configs.make(cfg, ncols=per_step)
+    if lk is not None:
+        _REF["op"] = reference_op(lk, cfg, w)
+        _REF["apply"] = lambda op, x, d: op.forward(x) if d == 0 else op.backward(x)
+        kind, what = "reference", f"linopkit (unmodified, {where})"
+    else:
+        from oracle import linop_oracle as orc
+
+        _REF["op"] = _oracle_op(cfg, w)
+        _REF["apply"] = orc.apply
+        kind, what = "port", "oracle port (reference package not importable)"
+    _REF["X"] = w.X
+    # one column per process; the operator is built once and shared copy-on-write
+    with mp.get_context("fork").Pool(per_step) as pool:
+        for _ in range(max(1, args.warmup)):
+            pool.map(_ref_column, range(per_step))  # plan caches, page-in
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            pool.map(_pool_column, range(per_step))
+            pool.map(_ref_column, range(per_step))
         dt = time.perf_counter() - t0
     value = 2 * per_step * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPES[cfg],
         "data": "synthetic (seeded numpy, SURVEY.md §8d)",
-        "config": {"workload": name, "columns_per_step": 2 * per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step, "kind": "port",
-                         "sample": f"{per_step} columns per step (one process per column), forward+backward, "
-                                   f"numpy port of the reference algorithm (oracle/linop_oracle.py)"},
+        "config": {"workload": NAMES[cfg], "global_columns": FULL_COLS[cfg], "columns_per_step": per_step,
+                   "step": "forward + backward of each sampled column, one host process per column"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step, "kind": kind,
+                         "sample": f"{per_step} of {FULL_COLS[cfg]} columns per step (one process per column, "
+                                   f"{per_step} of {ncpu} host threads), forward + backward through {what}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
 
 
-# --------------------------------------------------------------- GPU leg -----
+# ---------------------------------------------------------- GPU helpers -----
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -201,7 +336,6 @@ class ClockSampler:
             self.proc = None
             return self
         # the timed region starts only once the sampler is producing lines
-        # (short regions, e.g. 20 steps of C2 = 27 ms, still get samples)
         t0 = time.time()
         while time.time() - t0 < 5.0:
             if self.path.exists() and self.path.stat().st_size > 0:
@@ -224,8 +358,6 @@ class ClockSampler:
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = self.path.read_text().splitlines()
-        # samples taken after the timed region began (keep the last pre-region
-        # sample when the region was shorter than the sampling interval)
         lines = lines[max(0, getattr(self, "skip", 0) - 1):]
         for line in lines:
             f = [t.strip() for t in line.split(",")]
@@ -242,8 +374,7 @@ class ClockSampler:
         self.path.unlink(missing_ok=True)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def _peaks():
@@ -252,43 +383,6 @@ def _peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
-
-
-def _pass_bytes(cfg: int, label: str, ncols: int) -> int | None:
-    """Algorithmic HBM bytes of one launch of the labelled pass (SURVEY.md §8d
-    units: each operand block read or written once, vectors once).  Labels are
-    smat_apply_profiled's: kernel_length[_spec][_tw|_twin][_msk]."""
-    K = ncols
-    if cfg == 1:
-        return 2 * 1024 * K * 8
-    if cfg == 2:
-        n = 1 << 20
-        return 2 * n * K * 8 + (n * 8 if "_spec" in label else 0)
-    if cfg == 3:
-        return None  # compute-bound (single tile pass per column pair), no HBM roofline
-    if cfg == 4:
-        return 2 * (1 << 21) * K * 8
-    if cfg == 5:
-        n = configs_c5_n()
-        M = 1 << (2 * n - 1).bit_length()
-        P = 1 << max(0, (n - 1).bit_length())
-        e = 16
-        if label.startswith("wht_"):
-            return (n + P) * K * e
-        if label == "lowrank_contract":
-            return n * K * e + n * 32 * e
-        if label == "lowrank_expand":
-            return n * 32 * e + 2 * n * K * e
-        if "_spec" in label:
-            return 2 * M * K * e + M * e
-        if label.startswith("fft_c128_"):  # Bluestein outer passes: n-row side, M-row side, chirp
-            return n * K * e + M * K * e + n * e
-    return None
-
-
-def configs_c5_n():
-    from paper_1710_09578_b200 import configs
-    return configs.C5_N
 
 
 def _traffic(workload: str, kernel: str):
@@ -301,143 +395,237 @@ def _traffic(workload: str, kernel: str):
         return None
 
 
-def run_native(args, cfg):
+def pass_bytes(cfg: int, label: str, K: int) -> int | None:
+    """Algorithmic HBM bytes of one launch of the labelled pass (SURVEY.md §8d
+    units: every operand block read or written once, parameters once)."""
+    from paper_1710_09578_b200 import configs
+
+    if cfg == 1:
+        return 2 * 1024 * K * 8
+    if cfg == 2:
+        n = 1 << 20
+        return 2 * n * K * 8 + (n * 8 if "_spec" in label else 0)
+    if cfg == 3:
+        return None
+    if cfg == 4:
+        return 2 * (1 << 21) * K * 8
+    n = configs.C5_N
+    M = 1 << (2 * n - 1).bit_length()
+    P = 1 << max(0, (n - 1).bit_length())
+    e = 16
+    if label == "wht_lowrank_a":  # user side (n rows) + T1 (P rows) + V (n x 32)
+        return (n + P) * K * e + n * 32 * e
+    if label == "wht_lowrank_b":  # T1 + T2 (P rows each) + U~ (P x 32)
+        return 2 * P * K * e + P * 32 * e
+    if label.startswith("wht_"):
+        return 2 * P * K * e
+    if label == "lowrank_finalize":
+        return None
+    if "_spec" in label:
+        return 2 * M * K * e + M * e
+    if label.startswith("fft_c128_"):  # Bluestein outer passes: n-row or P-row side, M-row side, chirp
+        return P * K * e + M * K * e + n * e
+    return None
+
+
+def _graph_step(step, enabled: bool):
+    """Capture one step into a CUDA graph (returns (replay, outputs, mode))."""
+    import torch
+
+    if not enabled:
+        return step, None, "eager"
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            outs = step()
+        g.replay()
+        torch.cuda.synchronize()
+        return g.replay, outs, "cuda_graph"
+    except Exception as e:  # pragma: no cover - capture failure falls back to eager launches
+        _log(f"graph capture failed ({e}); eager launches")
+        torch.cuda.synchronize()
+        return step, None, "eager"
+
+
+def measure_config(cfg, w, op, X, dev, args, steps, warmup, graph=True, clocks=False):
+    """Device timing of fwd + bwd on the resident block X; returns a dict with
+    the step time, per-launch profile and the outputs of the timed step."""
     import torch
     import torch.distributed as dist
 
-    import paper_1710_09578_b200 as sm
-    from paper_1710_09578_b200 import configs
-
-    rank, world, local = _dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
-    name, dtype, _ = _workload_config(cfg)
-    w = configs.make(cfg)
-    op = configs.operator(cfg, w)
-    K = w.ncols
-    X = torch.from_numpy(np.ascontiguousarray(w.X)).to(f"cuda:{dev}")
-    del w.X
-    stream = torch.cuda.current_stream(dev)
-
-    flush = None
-    if cfg == 1:  # working set < L2: flush between timed steps
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    rank, world, _ = _dist_env()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}") if cfg == 1 else None
+    outs = {}
 
     def step():
-        if flush is not None:
-            flush.fill_(1)
         y = op.forward(X)
-        return op.backward(y)
+        z = op.backward(y)
+        outs["y"], outs["z"] = y, z
+        return y, z
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
+    torch.cuda.synchronize()
+    run, gouts, mode = _graph_step(step, graph)
+    if gouts is not None:
+        outs["y"], outs["z"] = gouts
+    stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    sampler = ClockSampler(dev) if clocks else None
+    if sampler:
+        sampler.__enter__()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(steps):
+        if flush is not None:
+            flush.fill_(1)
+        run()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__(None, None, None)
     ms = ev0.elapsed_time(ev1)
     if flush is not None:  # subtract the flush writes, timed separately
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             flush.fill_(1)
         f1.record(stream)
         torch.cuda.synchronize()
         ms -= f0.elapsed_time(f1)
-    t = torch.tensor([ms], device=f"cuda:{dev}", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
-    value = world * 2 * K / (ms_step / 1e3)
+    return {"ms": ms, "mode": mode, "y": outs["y"], "z": outs["z"], "clocks": sampler.summary() if sampler else None}
 
-    # per-launch durations (CUDA events on the launching stream) for the roofline
+
+def kernel_profile(cfg, op, X, dev, K, reps=3):
+    """Per-launch durations (CUDA events on the launching stream) of `reps`
+    eager fwd + bwd applies: {label: [ms, ...]}."""
+    import torch
+
     plan = op.plan_for(w_dtype(cfg), dev)
-    pcode = plan.dtype_code
-    xcode = pcode
+    stream = torch.cuda.current_stream(dev)
     Y = op.forward(X)
-    launches = {0: plan.launches(0, K), 1: plan.launches(1, K)}
-    prof = []
-    for _ in range(max(3, min(args.steps, 10))):
-        prof += [("fwd",) + p for p in plan.apply_profiled(0, X, xcode, Y, K, stream.cuda_stream)]
-        Z = torch.empty_like(X)
-        prof += [("bwd",) + p for p in plan.apply_profiled(1, Y, xcode, Z, K, stream.cuda_stream)]
-    by_kernel = {}
-    for d, lab, t_ms in prof:
-        by_kernel.setdefault(lab, []).append(t_ms)
-    total = sum(sum(v) for v in by_kernel.values())
-    peak, peak_src = _peaks()
-    # per-pass breakdown, and the roofline of the dominant kernel: the kernel
-    # family (precision + length, e.g. fft_c64_1024, all its fused variants)
-    # with the largest share of the step; achieved = its algorithmic bytes per
-    # launch over its mean launch time
+    Z = torch.empty_like(X)
+    by = {}
+    for _ in range(reps):
+        for lab, t in plan.apply_profiled(0, X, plan.dtype_code, Y, K, stream.cuda_stream):
+            by.setdefault(lab, []).append(t)
+        for lab, t in plan.apply_profiled(1, Y, plan.dtype_code, Z, K, stream.cuda_stream):
+            by.setdefault(lab, []).append(t)
+    return plan, by
+
+
+def roofline_of(cfg, workload, by, K, ms_step, reps, peak, peak_src, fp64_peak=None):
+    """Dominant single kernel (largest share of the step) and the step-level fractions."""
+    from paper_1710_09578_b200 import configs
+
+    total = sum(sum(v) for v in by.values())
     passes = {}
-    for lab, ts in by_kernel.items():
-        pb = _pass_bytes(cfg, lab, K)
+    for lab, ts in by.items():
+        pb = pass_bytes(cfg, lab, K)
         avg = float(np.mean(ts))
-        passes[lab] = {"launches_per_step": len(ts) / max(3, min(args.steps, 10)), "avg_ms": avg,
-                       "bytes_per_launch": pb, "GB/s": (pb / (avg / 1e3) / 1e9) if pb else None}
-
-    def family(lab):
-        parts = lab.split("_")
-        return "_".join(parts[:3]) if lab.startswith("fft_") else lab
-
-    fams = {}
-    for lab, ts in by_kernel.items():
-        fams.setdefault(family(lab), []).append(lab)
-    dom = max(fams, key=lambda f: sum(sum(by_kernel[l]) for l in fams[f]))
-    dom_t = sum(sum(by_kernel[l]) for l in fams[dom])
-    dom_n = sum(len(by_kernel[l]) for l in fams[dom])
-    roofline = None
-    if all(_pass_bytes(cfg, l, K) is not None for l in fams[dom]):
-        dom_b = sum(_pass_bytes(cfg, l, K) * len(by_kernel[l]) for l in fams[dom])
-        pb = dom_b / dom_n
-        dom_avg_ms = dom_t / dom_n
-        achieved = pb / (dom_avg_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dom, "variants": sorted(fams[dom]), "achieved": achieved,
-                    "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": _traffic(args.workload, dom),
-                    "bytes_per_launch": pb, "avg_launch_ms": dom_avg_ms,
-                    "share_of_step": dom_t / total if total else None,
-                    "peak_source": peak_src,
-                    # the north star's "~8 TB/s" nominal B200 HBM3e peak
-                    "frac_vs_nominal_8000": achieved / 8000.0}
-    if cfg == 3:
-        # FP32-bound config: algorithmic FFT flops of the
-        # length-8192 embedding with real-pair packing, whole step, against the
-        # nominal FP32 FFMA peak
-        flops = 2 * configs.c3_flops_per_direction(K)
-        achieved = flops / (ms_step / 1e3) / 1e12
-        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        roofline = {"bound": "fp32", "kernel": "all fft_c64 passes of the step", "variants": sorted(by_kernel),
-                    "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                    "traffic": None, "flops_per_step": flops,
-                    "peak_source": "nominal FP32 FFMA: 148 SMs x 128 lanes x 2 flops x 1965 MHz"}
+        passes[lab] = {"launches_per_step": len(ts) / reps, "avg_ms": avg, "bytes_per_launch": pb,
+                       "GB/s": (pb / (avg / 1e3) / 1e9) if pb else None,
+                       "frac": (pb / (avg / 1e3) / 1e9 / peak) if pb else None,
+                       "share_of_step": sum(ts) / total if total else None}
     alg = configs.algorithmic_bytes(cfg, K)
-    transform_gbs = 2 * alg / (ms_step / 1e3) / 1e9
+    step_gbs = 2 * alg / (ms_step / 1e3) / 1e9
+    rf = {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+          "step_level": {"achieved": step_gbs, "frac": step_gbs / peak, "bytes_per_step": 2 * alg,
+                         "definition": "algorithmic bytes of the minimal-pass plan (SURVEY.md §8d) per step / "
+                                       "device step time"}}
+    cands = [l for l in by if pass_bytes(cfg, l, K)]
+    if cands:
+        dom = max(cands, key=lambda l: sum(by[l]))
+        rf.update({"kernel": dom, "achieved": passes[dom]["GB/s"], "frac": passes[dom]["frac"],
+                   "traffic": _traffic(workload, dom), "bytes_per_launch": passes[dom]["bytes_per_launch"],
+                   "avg_launch_ms": passes[dom]["avg_ms"], "share_of_step": passes[dom]["share_of_step"],
+                   "frac_vs_nominal_8000": passes[dom]["GB/s"] / 8000.0})
+    else:
+        rf.update({"kernel": None, "achieved": step_gbs, "frac": step_gbs / peak, "traffic": None})
+    if cfg == 3 and fp64_peak is not None:
+        fl = 2 * configs.c3_flops_per_direction(K)
+        ach = fl / (ms_step / 1e3) / 1e12
+        rf["fp32"] = {"achieved": ach, "peak": fp64_peak["ffma2_fp32"], "unit": "TFLOP/s",
+                      "frac": ach / fp64_peak["ffma2_fp32"], "flops_per_step": fl,
+                      "peak_source": "measured FFMA2 (smat_probe_peak kind 3, this box)"}
+    if cfg == 5 and fp64_peak is not None:
+        fl = 2 * configs.c5_flops_per_direction(K)
+        ach = fl / (ms_step / 1e3) / 1e12
+        pk = max(fp64_peak["dfma_fp64"], fp64_peak["dmma_fp64"])
+        rf["fp64"] = {"achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "flops_per_step": fl,
+                      "peak_source": "measured max(DFMA, DMMA) FP64 peak of this box (smat_probe_peak; "
+                                     "the two share one pipe)",
+                      "definition": "algorithmic FP64 flops per step (SURVEY.md §8d: FFT 5 M log2 M x2, "
+                                    "rank-32 halves 8 n r x2, FWHT 2 P log2 P, diagonals) / device step time"}
+    return rf, passes
 
-    # end-to-end through the public API with pinned host buffers
+
+def w_dtype(cfg):
+    return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
+
+
+def probe_peaks(dev):
+    from paper_1710_09578_b200 import _native
+
+    names = ["dfma_fp64", "dmma_fp64", "dfma_plus_dmma_fp64", "ffma2_fp32"]
+    return {n: _native.probe_peak(k, dev) for k, n in enumerate(names)}
+
+
+# ------------------------------------------------------------- GPU leg ------
+def run_native(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_09578_b200 import configs, sharding
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.cuda.current_device()
+    peak, peak_src = _peaks()
+    w = configs.make(cfg)
+    op = configs.operator(cfg, w)
+    K = w.ncols
+    a, b = sharding.column_slices(K, world)[rank]
+    Kl = b - a
+    Xh_local = np.ascontiguousarray(w.X[:, a:b])
+    X = torch.from_numpy(Xh_local).to(f"cuda:{dev}")
+
+    m = measure_config(cfg, w, op, X, dev, args, args.steps, args.warmup, graph=not args.no_graph, clocks=True)
+
+    # parity gate on the outputs of the timed step (this rank's checked columns)
+    par = rank_parity(cfg, w, a, b, args.parity_cols, lambda loc: (m["y"][:, loc].cpu().numpy(),
+                                                                   m["z"][:, loc].cpu().numpy()))
+    ms_max, parity = reduce_over_ranks(m["ms"], par, cfg, world, f"cuda:{dev}")
+    ms_step = ms_max / args.steps
+    value = 2 * K / (ms_step / 1e3)
+
+    # per-launch profile and rooflines (eager, events on the launching stream)
+    fp_peaks = probe_peaks(dev) if rank == 0 else None
+    reps = 3
+    plan, by = kernel_profile(cfg, op, X, dev, Kl, reps)
+    rf, passes = roofline_of(cfg, args.workload, by, Kl, ms_step * 1.0, reps, peak, peak_src, fp_peaks)
+    launches = plan.launches(0, Kl) + plan.launches(1, Kl)
+
+    # end to end through the public API with pinned HOST buffers
     e2e = None
     if not args.no_e2e:
-        Xh = X.cpu().pin_memory()
-        e_steps = max(3, min(args.steps, 5))
-        # two untimed steps in the timed loop's exact pattern, so the pinned
-        # host caching allocator holds every output block the loop cycles through
-        for _ in range(2):
+        Xh = torch.from_numpy(Xh_local).pin_memory()
+        e_steps = 3
+        for _ in range(2):  # the pinned caching allocator holds the blocks the loop cycles through
             yh = op.forward(Xh)
             zh = op.backward(yh)
         torch.cuda.synchronize()
@@ -449,297 +637,103 @@ def run_native(args, cfg):
             zh = op.backward(yh)
         dt = time.perf_counter() - t0
         tt = torch.tensor([dt], device=f"cuda:{dev}", dtype=torch.float64)
+        bi = torch.tensor([Xh.numel() * Xh.element_size() + yh.numel() * yh.element_size()], device=f"cuda:{dev}",
+                          dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dist.all_reduce(bi, op=dist.ReduceOp.SUM)
         dt = float(tt.item())
-        bytes_in = Xh.numel() * Xh.element_size() + yh.numel() * yh.element_size()
-        bytes_out = yh.numel() * yh.element_size() + zh.numel() * zh.element_size()
-        e2e = {"value": world * 2 * K * e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(bytes_in),
-               "d2h_bytes_per_step": int(bytes_out), "steps": e_steps,
-               "path": "op.forward/op.backward on pinned CPU tensors (smat_apply_host, chunked H2D/compute/D2H)"}
+        nb = int(bi.item())
+        e2e = {"value": 2 * K * e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+               "steps": e_steps,
+               "path": "op.forward / op.backward on pinned CPU tensors (smat_apply_host: chunked pitched H2D, "
+                       "device passes, D2H on three streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg)
 
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        per_config = {}
+        for c2 in (1, 2, 3, 4, 5):
+            if c2 == cfg:
+                continue
+            try:
+                per_config[f"c{c2}"] = _per_config(c2, dev, peak, peak_src, fp_peaks, not args.no_graph)
+            except Exception as e:  # pragma: no cover - report, never hide the headline
+                per_config[f"c{c2}"] = {"error": repr(e)}
+            torch.cuda.empty_cache()
+
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded numpy, SURVEY.md §8d)",
-            "config": {"workload": name, "columns_per_step": 2 * K, "global_columns": world * K,
-                       "parallelism": f"column-sharded x{world} (no data-path collective)",
+            "metric": METRIC, "value": value if parity["pass"] else None, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPES[cfg],
+            "data": "synthetic (seeded numpy, SURVEY.md §8d)",
+            "config": {"workload": NAMES[cfg], "global_columns": K,
+                       "columns_per_rank": [e - s for s, e in sharding.column_slices(K, world)],
+                       "parallelism": f"column slices x{world} (strong scaling, no data-path collective)",
                        "l2": "inputs larger than L2" if cfg != 1 else "L2 flushed between steps (256 MB write)",
-                       "step": "forward + backward over the whole block"},
-            "transform_gbs": transform_gbs,
-            "algorithmic_bytes_per_direction": alg,
-            "roofline": roofline,
+                       "step": "forward + backward over the whole block", "launch": m["mode"]},
+            "transform_gbs": rf["step_level"]["achieved"],
+            "roofline": rf,
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(args.steps * (launches[0] + launches[1])),
-            "launches_per_step": {"forward": launches[0], "backward": launches[1]},
-            "kernels_ms_per_step": {k: float(np.sum(v)) / max(3, min(args.steps, 10)) for k, v in by_kernel.items()},
+            "gpu_launches": int(args.steps * launches),
+            "launches_per_step": launches,
             "passes": passes,
+            "measured_peaks_tflops": fp_peaks,
+            "per_config": per_config,
             "plan": plan.describe(),
-            "clocks": clk.summary(),
+            "clocks": m["clocks"],
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-# ------------------------------------------------- solver leg ----
-def run_solver(args):
-    """--workload cg: conjugate gradients on the normal equations of C2's
-    operator (Circulant 2^20, 64 right-hand sides, complex128 as the
-    reference's cg_solve computes), fixed iteration count.  One step = one CG
-    iteration over all 64 columns: A p and A^H (A p) through the compiled plan
-    plus the fused step kernels, replayed from a CUDA graph."""
-    import torch
-    import torch.distributed as dist
-
-    import paper_1710_09578_b200 as sm
-    from paper_1710_09578_b200 import configs, solvers
-
-    rank, world, local = _dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
-    w = configs.make(2)
-    op = sm.Circulant(w.params["c"])
-    K = w.ncols
-    rhs = torch.from_numpy(np.ascontiguousarray(w.X)).to(f"cuda:{dev}").to(torch.complex128)
-    del w.X
-    opts_w = sm.SolveOptions(max_iterations=args.warmup, relative_tolerance=1e-300)
-    sm.cg_solve(op, rhs, opts_w)  # warm-up: plans, workspaces, graph capture path
-    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    opts = sm.SolveOptions(max_iterations=args.steps, relative_tolerance=1e-300)
-    stream = torch.cuda.current_stream(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        rep = sm.cg_solve(op, rhs, opts)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device=f"cuda:{dev}", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_it = float(t.item()) / args.steps
-    n = 1 << 20
-    e = 16
-    # per iteration: two 3-pass c128 convolutions (read+write of the block per
-    # pass + spectrum) and the step kernels (p.ap reduce 2 blocks, x/r update
-    # 4 read + 2 write, p update 2 read + 1 write)
-    conv = 3 * 2 * n * K * e + n * e
-    step_bytes = (2 + 6 + 3) * n * K * e
-    it_bytes = 2 * conv + step_bytes
-    peak, peak_src = _peaks()
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import linop_oracle as orc
-
-        its = 4
-        t0 = time.perf_counter()
-        orc.cg_solve(orc.circulant(configs.make(2, ncols=1).params["c"]), np.asarray(rhs[:, :1].cpu()),
-                     max_iterations=its, tol=1e-300)
-        dt = time.perf_counter() - t0
-        cpu = {"value": its / dt, "unit": "column-iterations/s", "cores": 1, "kind": "port",
-               "sample": f"1 of {K} columns, {its} iterations, numpy oracle of solvers.py:75-106 ({dt:.2f} s)"}
-    if rank == 0:
-        line = {
-            "metric": "CG column-iterations/s (normal equations)", "value": world * K / (ms_it / 1e3),
-            "unit": "column-iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_it, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c128", "data": "synthetic (seeded numpy, C2 operator and block, SURVEY.md §8d)",
-            "config": {"workload": "cg_solve(Circulant(2^20), 2^20x64 complex128, normal equations)",
-                       "step": "one CG iteration over all 64 columns (A p, A^H A p, fused step kernels)",
-                       "l2": "inputs larger than L2", "graph": solvers.last_loop_mode},
-            "roofline": {"bound": "hbm", "kernel": "whole iteration", "achieved": it_bytes / (ms_it / 1e3) / 1e9,
-                         "peak": peak, "unit": "GB/s", "frac": it_bytes / (ms_it / 1e3) / 1e9 / peak,
-                         "traffic": None, "bytes_per_launch": it_bytes, "peak_source": peak_src},
-            "iterations_run": int(np.max(rep.iterations)),
-            "cpu_baseline": cpu,
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
         dist.destroy_process_group()
+    return 0 if parity["pass"] else 1
 
 
-def _ista_problem(size: int, seed: int = 1710):
-    """The reference bench's ISTA scenario (pkg/src/linopkit/bench.py:142-162)
-    restated: Partial(Hadamard(log2 m), rows) . Circulant(c), m = 2 size,
-    size/16-sparse truth; returns (operator factors, b, lam) in numpy."""
-    rng = np.random.default_rng([seed, size])
-    m = 2 * size
-    rows = rng.choice(m, size=size, replace=False)
-    c = rng.standard_normal(m) / np.sqrt(m)
-    xt = np.zeros(m)
-    sup = rng.choice(m, size=max(1, size // 16), replace=False)
-    xt[sup] = rng.standard_normal(sup.size) + np.sign(rng.standard_normal(sup.size))
-    return rows, c, xt
-
-
-def run_ista(args):
-    """--workload ista: the reference bench's ISTA scenario at size 2^20
-    (Partial(Hadamard(21), 2^20 rows) . Circulant(2^21), float64), a fixed step
-    size, `--steps` ISTA iterations on the device (one CUDA graph replayed).
-    value = ISTA iterations per second."""
+def _per_config(cfg, dev, peak, peak_src, fp_peaks, graph):
+    """Device-only line of another config: ms/step, roofline, parity of two columns."""
     import torch
 
-    import paper_1710_09578_b200 as sm
-    from paper_1710_09578_b200 import solvers
+    from paper_1710_09578_b200 import configs
 
-    torch.cuda.set_device(0)
-    size = 1 << 20
-    rows, c, xt = _ista_problem(size)
-    order = int(np.log2(2 * size))
-    op = sm.Product(sm.Partial(sm.Hadamard(order), row_indices=rows), sm.Circulant(c))
-    b = op.forward(xt)
-    lam = 0.02 * float(np.abs(op.backward(b)).max())
-    top = sm.power_iteration(op, mode="singular", tol=1e-6, max_iter=50, seed=0).value
-    alpha = 1.0 / (1.01 * top ** 2)
-    bd = torch.from_numpy(b).cuda()
-    sm.ista(op, bd, sm.IstaOptions(lam=lam, steps=max(1, args.warmup), step_size=alpha))  # warm-up + capture
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        res = sm.ista(op, bd, sm.IstaOptions(lam=lam, steps=args.steps, step_size=alpha))
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms_it = ev0.elapsed_time(ev1) / args.steps
-    cpu = None
-    if not args.no_cpu_baseline:
-        from oracle import linop_oracle as orc
-
-        oo = orc.product(orc.partial(orc.hadamard(order), rows), orc.circulant(c))
-        its = 2
-        t0 = time.perf_counter()
-        orc.ista(oo, b, lam, steps=its, step_size=alpha)
-        dt = time.perf_counter() - t0
-        cpu = {"value": its / dt, "unit": "iterations/s", "cores": 1, "kind": "port",
-               "sample": f"{its} ISTA iterations (+1 residual), numpy oracle of solvers.py:163-194 ({dt:.2f} s)"}
-    line = {
-        "metric": "ISTA iterations/s (reference bench ista scenario)", "value": 1e3 / ms_it,
-        "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_it,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, reference bench.py:142-162 shapes)",
-        "config": {"workload": "ista(Partial(Hadamard(21), 2^20 rows) . Circulant(2^21)), size 2^20",
-                   "step": "one ISTA iteration: forward, residual, backward, soft-threshold update",
-                   "graph": solvers.last_loop_mode},
-        "final_objective": float(res.objective_trace[-1]),
-        "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line), flush=True)
-
-
-def run_sparse(args):
-    """--workload sparse: Sparse (CSR) forward + backward of a 2^20 x 2^20
-    float64 operator with 16 random nonzeros per row (duplicates summed) on a
-    2^20 x 64 block — SURVEY.md §8(f) row 3 at scale.  HBM roofline: CSR
-    arrays once per direction, one x row (K values) gathered per nonzero, y
-    written once."""
-    import torch
-
-    import paper_1710_09578_b200 as sm
-
-    torch.cuda.set_device(0)
-    n, per_row, K = 1 << 20, 16, 64
-    rng = np.random.default_rng(1710_3)
-    rows = np.repeat(np.arange(n), per_row)
-    cols = rng.integers(0, n, n * per_row)
-    vals = rng.standard_normal(n * per_row)
-    S = sm.Sparse.__new__(sm.Sparse)  # bulk constructor: arrays instead of a triplet list
-    sm.Sparse._from_arrays(S, n, n, rows, cols, vals)
-    X = torch.from_numpy(rng.standard_normal((n, K))).cuda()
-
-    def step():
-        return S.backward(S.forward(X))
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    nnz = S.nnz
-    # compulsory bytes per direction: CSR arrays, x and y once each (the
-    # gathered x rows mostly hit L2 here; counting one DRAM row per nonzero
-    # instead gives the `gather_model` upper bound)
-    per_dir = nnz * (8 + 8) + (n + 1) * 8 + 2 * n * K * 8
-    gather_dir = nnz * (8 + 8) + (n + 1) * 8 + nnz * K * 8 + n * K * 8
-    peak, peak_src = _peaks()
-    cpu = None
-    if not args.no_cpu_baseline:
-        from oracle import linop_oracle as orc
-
-        cols_s = 2
-        tri = list(zip(rows.tolist(), cols.tolist(), vals.tolist()))
-        oo = orc.sparse(n, n, tri)
-        xs = X[:, :cols_s].cpu().numpy()
-        t0 = time.perf_counter()
-        orc.apply(oo, orc.apply(oo, xs, 0), 1)
-        dt = time.perf_counter() - t0
-        cpu = {"value": 2 * cols_s / dt, "unit": "columns/s", "cores": 1, "kind": "port",
-               "sample": f"{cols_s} of {K} columns, forward then backward, numpy CSR oracle ({dt:.2f} s)"}
-    line = {
-        "metric": "Sparse fwd/bwd columns/s", "value": 2 * K / (ms / 1e3), "unit": "columns/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform CSR)",
-        "config": {"workload": f"Sparse({n}x{n}, nnz {nnz}) on {n}x{K} float64",
-                   "step": "forward + backward (conjugate-transposed CSR)"},
-        "roofline": {"bound": "hbm", "kernel": "csr_kernel", "achieved": 2 * per_dir / (ms / 1e3) / 1e9,
-                     "peak": peak, "unit": "GB/s", "frac": 2 * per_dir / (ms / 1e3) / 1e9 / peak, "traffic": None,
-                     "bytes_per_launch": per_dir, "peak_source": peak_src,
-                     "gather_model_GBps": 2 * gather_dir / (ms / 1e3) / 1e9},
-        "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line), flush=True)
-
-
-def w_dtype(cfg):
-    return {1: np.float64, 2: np.complex64, 3: np.float32, 4: np.complex64, 5: np.complex128}[cfg]
+    w = configs.make(cfg)
+    op = configs.operator(cfg, w)
+    K = w.ncols
+    X = torch.from_numpy(np.ascontiguousarray(w.X)).to(f"cuda:{dev}")
+    m = measure_config(cfg, w, op, X, dev, None, 10, 3, graph=graph)
+    ms_step = m["ms"] / 10
+    cols = [0, K - 1]
+    par = check_parity(cfg, w, _oracle_op(cfg, w), np.ascontiguousarray(w.X[:, cols]),
+                       m["y"][:, cols].cpu().numpy(), m["z"][:, cols].cpu().numpy(), cols)
+    plan, by = kernel_profile(cfg, op, X, dev, K, 3)
+    rf, _ = roofline_of(cfg, f"c{cfg}", by, K, ms_step, 3, peak, peak_src, fp_peaks)
+    return {"workload": NAMES[cfg], "dtype": DTYPES[cfg], "ms_per_step": ms_step, "value": 2 * K / (ms_step / 1e3),
+            "unit": UNIT, "roofline": rf, "parity": par, "launch": m["mode"],
+            "kernels_ms_per_step": {k: float(np.sum(v)) / 3 for k, v in by.items()}}
 
 
 def main():
     args = _args()
-    if args.workload == "cg":
-        run_solver(args)
-        return
-    if args.workload == "ista":
-        run_ista(args)
-        return
-    if args.workload == "sparse":
-        run_sparse(args)
-        return
+    if args.workload in ("cg", "ista", "sparse"):
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_extra
+
+        {"cg": bench_extra.run_solver, "ista": bench_extra.run_ista, "sparse": bench_extra.run_sparse}[
+            args.workload](args)
+        return 0
     cfg = int(args.workload[1])
     if args.impl == "reference":
-        run_reference(args, cfg)
-    else:
-        run_native(args, cfg)
+        return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _launch_ranks(args)
+    return run_native(args, cfg)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -129,6 +129,19 @@ def c3_flops_per_direction(ncols: int) -> float:
     return (ncols / 2) * per_pair
 
 
+def c5_flops_per_direction(ncols: int, n: int | None = None) -> float:
+    """~1.02 G FP64 flops per column of C5 — the length-M
+    Bluestein FFT and inverse FFT (5 M log2 M each), the spectrum and chirp /
+    diagonal multiplies (6 flops per complex product), the two rank-32 halves
+    (8 n r each) and the padded FWHT (2 P log2 P)."""
+    N = C5_N if n is None else n
+    M = 1 << (2 * N - 1).bit_length()
+    P = 1 << max(0, (N - 1).bit_length())
+    lm, lp = M.bit_length() - 1, P.bit_length() - 1
+    per_col = 2 * 5 * M * lm + 6 * M + 2 * 6 * N + 2 * 8 * N * 32 + 2 * P * lp
+    return float(ncols) * per_col
+
+
 def algorithmic_bytes(cfg: int, ncols: int, n: int | None = None) -> int:
     """Bytes of the minimal number of HBM passes per direction."""
     if cfg == 1:

@@ -46,15 +46,7 @@ HOST_CHUNK_BYTES = 256 << 20
 
 
 def _host_chunk(ncols: int, n_in: int, n_out: int, esz: int) -> int:
-    """Columns per host-path chunk (0 = one contiguous DMA each way).
-
-    SMAT_HOST_CHUNK_COLS=c forces c columns per chunk (0: no chunking)."""
-    import os
-
-    forced = os.environ.get("SMAT_HOST_CHUNK_COLS")
-    if forced:
-        c = int(forced)
-        return c if 0 < c < ncols else 0
+    """Columns per host-path chunk (0 = one contiguous DMA each way)."""
     if max(n_in, n_out) * ncols * esz < HOST_CHUNK_BYTES:
         return 0
     for row_bytes in (512, 256, 128):

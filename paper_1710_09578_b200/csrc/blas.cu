@@ -1,11 +1,6 @@
-// blas.cu — the two plain complex128 GEMMs of a rank-r LowRank term through
-// cuBLAS (library GEMMs: the contraction W = F^H X, a tall-skinny reduction
-// over ~1e6 rows, and the expansion Y += G W).  On this B200 the library's
-// FP64 GEMMs beat the hand-written DFMA kernels of lowrank.cu for C5's shapes
-// (tools/zgemm_probe.py: contraction 0.78 ms with the Gauss 3-multiply
-// ZGEMM3M vs 1.45 ms; expansion 1.37 vs 1.58 ms), so complex128 LowRank terms
-// use them; the kernels of lowrank.cu remain for complex64 and as the
-// SMAT_LR_BLAS=0 path.
+// blas.cu — the Dense (Matrix) leaf as a plain library GEMM through cuBLAS
+// (reference leaves.py:40-46: entries @ x).  No structured transform and no
+// LowRank term uses it (those run on the hand-written kernels).
 //
 // cuBLAS is resolved at run time (dlopen of libcublas.so.12 — the copy torch
 // has already loaded, else the toolkit's), so libsmat.so has no link-time
@@ -38,7 +33,6 @@ struct Blas {
   SetStreamFn set_stream = nullptr;
   SetWsFn set_ws = nullptr;
   ZgemmFn zgemm = nullptr;
-  ZgemmFn zgemm3m = nullptr;
   GemmAny sgemm = nullptr, dgemm = nullptr, cgemm = nullptr;
 };
 
@@ -46,8 +40,6 @@ const Blas& blas() {
   static Blas b;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* e = getenv("SMAT_LR_BLAS");
-    if (e && e[0] == '0') return;
     void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return;
@@ -55,11 +47,10 @@ const Blas& blas() {
     b.set_stream = (SetStreamFn)dlsym(h, "cublasSetStream_v2");
     b.set_ws = (SetWsFn)dlsym(h, "cublasSetWorkspace_v2");
     b.zgemm = (ZgemmFn)dlsym(h, "cublasZgemm_v2");
-    b.zgemm3m = (ZgemmFn)dlsym(h, "cublasZgemm3m");
     b.sgemm = (GemmAny)dlsym(h, "cublasSgemm_v2");
     b.dgemm = (GemmAny)dlsym(h, "cublasDgemm_v2");
     b.cgemm = (GemmAny)dlsym(h, "cublasCgemm_v2");
-    b.ok = b.create && b.set_stream && b.set_ws && b.zgemm && b.zgemm3m && b.sgemm && b.dgemm && b.cgemm;
+    b.ok = b.create && b.set_stream && b.set_ws && b.zgemm && b.sgemm && b.dgemm && b.cgemm;
   });
   return b;
 }
@@ -98,22 +89,6 @@ bool blas_available() { return blas().ok; }
 // call inside a CUDA-graph capture allocates nothing
 void blas_warm(int device) {
   if (blas().ok) handle_for(device);
-}
-
-// Column-major C (m x n, ldc) = alpha op(A) op(B) + beta C, complex128;
-// op: 0 = N, 2 = C (conjugate transpose).  gauss3m: the 3-multiply variant.
-void blas_zgemm(int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
-                int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc, bool gauss3m) {
-  const Blas& b = blas();
-  SMAT_CHECK(b.ok, SMAT_UNSUPPORTED, "cuBLAS not available");
-  SMAT_CHECK(m < (int64_t(1) << 31) && n < (int64_t(1) << 31) && k < (int64_t(1) << 31), SMAT_UNSUPPORTED,
-             "zgemm dimension exceeds int32");
-  Handle h = handle_for(device);
-  bind_stream(h, device, s);
-  const double2 one = make_double2(1.0, 0.0), beta = make_double2(beta_re, 0.0);
-  const int st = (gauss3m ? b.zgemm3m : b.zgemm)(h, opa, opb, int(m), int(n), int(k), &one, (const double2*)A,
-                                                 int(lda), (const double2*)B, int(ldb), &beta, (double2*)C, int(ldc));
-  SMAT_CHECK(st == 0, SMAT_CUDA_ERROR, "cublasZgemm failed with status " + std::to_string(st));
 }
 
 // Column-major C = op(A) op(B) + beta C in the plan dtype (float32, float64,

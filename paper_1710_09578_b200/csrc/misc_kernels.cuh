@@ -91,20 +91,14 @@ struct LowRankArgs {
   const void* s = nullptr;  // r or null
   int32_t s_conj = 0, accumulate = 0;
   int64_t rows = 0, r = 0, K = 0, ldx = 0, ldy = 0;
-  // blocked four-step row layout of the block side (x for contract, y for
-  // expand) when rm_n1 > 0: logical row r = n1 + rm_n1*k2 is stored at row
-  // ((n1 / 64) * rm_n2b + k2) * 64 + n1 % 64 (rm_n1 a multiple of 64)
-  int64_t rm_n1 = 0, rm_n2b = 0;
 };
-// cuBLAS complex128 GEMM (blas.cu): column-major C (m x n) = op(A) op(B) +
-// beta C, op 0 = N / 2 = C; resolved at run time, blas_available() false when
-// libcublas cannot be loaded (or SMAT_LR_BLAS=0)
+// cuBLAS GEMM (blas.cu), the Dense leaf's plain library GEMM: column-major
+// C (m x n) = op(A) op(B) + beta C, op 0 = N / 2 = C; resolved at run time,
+// blas_available() false when libcublas cannot be loaded
 bool blas_available();
 void blas_warm(int device);
 void blas_gemm(int dt, int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
                int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc);
-void blas_zgemm(int device, cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A,
-                int64_t lda, const void* B, int64_t ldb, double beta_re, void* C, int64_t ldc, bool gauss3m);
 
 // number of launches (dry) or launch
 int launch_lowrank_contract(int dt, const LowRankArgs& a, int device, cudaStream_t s, bool dry);

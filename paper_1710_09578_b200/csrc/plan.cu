@@ -139,18 +139,13 @@ void Ctx::join(cudaStream_t side) {
 
 // Whether a transform of length Nt runs as a four-step decomposition (else one
 // tile pass).  Beyond one tile always; single-precision convolutions of more
-// than SMAT_FOURSTEP_C64CONV points (default 2048) too: a one-tile 4096-point
+// than 2048 points too: a one-tile 4096-point
 // convolution keeps only 4 columns per CTA and is load-latency bound, while
 // its 64 x 64 four-step runs three passes of 256-byte-row tiles (for C3 the
 // intermediate lives mostly in L2).
 static bool fourstep(int64_t Nt, bool conv, int cdt) {
-  static int64_t lim = -1;
-  if (lim < 0) {
-    const char* e = getenv("SMAT_FOURSTEP_C64CONV");
-    lim = e ? atoll(e) : 2048;
-  }
   if (Nt > kTileMax) return true;
-  return conv && cdt == SMAT_C64 && Nt > lim;
+  return conv && cdt == SMAT_C64 && Nt > 2048;
 }
 
 // Split of a four-step transform of length Nt = N1 * N2 (N1 = contiguous /
@@ -356,24 +351,10 @@ static void xform_pass_common(FftArgs& a, Ctx& c) {
   a.tw = twiddle4096(c.device, cplx_of(c.dt) == SMAT_C128);
 }
 
-static bool blocked_w() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SMAT_BLOCKED_W");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-
-static bool tw_in_pass3(bool dbl, int64_t N1) {
-  static int force = -2;
-  if (force == -2) {
-    const char* e = getenv("SMAT_TW_PASS3");
-    force = e ? (e[0] == '1' ? 1 : 0) : -1;
-  }
-  if (force >= 0) return force == 1;
-  return dbl && N1 >= 2048;
-}
+// The inverse four-step twiddle sits between pass 2's IFFT and pass 3; it
+// goes to pass 3's input when pass 2's tile has no shared memory left for it
+// (double precision, N1 >= 2048).
+static bool tw_in_pass3(bool dbl, int64_t N1) { return dbl && N1 >= 2048; }
 
 static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   const int cdt = cplx_of(c.dt);
@@ -434,7 +415,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   // per block, instead of both walking N1*K-element strides that put every
   // row in its own 2 MB page (translation-bound, tools/tma_probe.cu).  Only
   // the user-layout side of the outer passes stays strided.
-  const bool blk = O == 1 && N1 >= 128 && blocked_w();
+  const bool blk = O == 1 && N1 >= 128;
   SMAT_CHECK(blk || (!io.x_blk && !io.y_blk), SMAT_UNSUPPORTED, "blocked rows need the blocked four-step path");
   SMAT_CHECK(!io.y_blk || io.mid, SMAT_UNSUPPORTED, "blocked output rows need the convolution passes");
   constexpr int BL = 6;
@@ -499,9 +480,6 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.scale = io.scale; a.accumulate = io.acc;
     c.fft(cdt, int(N1), a);
   } else {
-    // The inverse four-step twiddle sits between pass 2's IFFT and pass 3; it
-    // goes to pass 3's input when pass 2's tile has no shared memory left for
-    // it (double precision, N1 >= 2048) or when forced by SMAT_TW_PASS3=0/1.
     const bool tw3 = tw_in_pass3(dbl, N1);
     // ---- pass 2 (convolution): W -> W
     {
@@ -1916,8 +1894,7 @@ struct Builder {
         // pruned halves only when each half is a single tile pass: once the
         // halves go four-step too, one four-step convolution of length L moves
         // fewer bytes (x read and y written once) in half the launches
-        const char* pe = getenv("SMAT_TOEPLITZ_PRUNE");
-        const bool prune = pe ? pe[0] == '1' : !fourstep(t->L / 2, true, cdt);
+        const bool prune = !fourstep(t->L / 2, true, cdt);
         if (prune && t->L > kTileMax && t->L / 2 <= kTileMax && std::max(n, m) <= t->L / 2) {
           const int64_t h = t->L / 2;
           DevBuf* se = new_buf(p, SMAT_C128, h);

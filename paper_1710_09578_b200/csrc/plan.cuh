@@ -134,12 +134,6 @@ struct Ctx {
     note("csr");
     if (!measure) launch_csr(dt, a, stream);
   }
-  // library GEMM (cuBLAS, complex128): not counted as one of the engine's launches
-  void zgemm(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
-             int64_t ldb, double beta, void* C, int64_t ldc, bool gauss3m, const char* label) {
-    note(label);
-    if (!measure) blas_zgemm(device, stream, opa, opb, m, n, k, A, lda, B, ldb, beta, C, ldc, gauss3m);
-  }
   void gemm_blas(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
                  int64_t ldb, double beta, void* C, int64_t ldc) {
     note("gemm_blas");

@@ -47,15 +47,6 @@ static bool launch_fft_tma_c128(int N, const FftArgs& a, cudaStream_t s) {
   }
 }
 
-static bool tma_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SMAT_NO_TMA");
-    on = (e && e[0] == '1') ? 0 : 1;
-  }
-  return on == 1;
-}
-
 void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
   // persistent TMA-fed variant first (large tiles, complex in and out)
   // (below 256 points only the four-step passes with twiddles / spectra /
@@ -63,7 +54,7 @@ void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
   const bool pad = (a.g_mod - 1) + (N - 1) * a.gin_stride >= a.n_valid_in;
   const bool trunc = (a.g_mod - 1) + (N - 1) * a.gout_stride >= a.n_valid_out;
   const bool extras = a.mid || a.tw_on || a.pre || a.post || pad || trunc;
-  if ((N >= 256 || (N >= 64 && extras)) && tma_enabled()) {
+  if (N >= 256 || (N >= 64 && extras)) {
     if (cdt == SMAT_C64 && launch_fft_tma_c64(N, a, s)) return;
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;
   }

@@ -78,15 +78,6 @@ template <class C, int N>
 constexpr bool kPdl = sizeof(C) == 8 && N <= 128;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-inline bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SMAT_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 // launcher-only flags of the TMA pass: the pre (post) vector is stored per
 // tile (pre_gmul / post_gmul) and rides with the tile as a bulk-loaded slice
 enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21 };
@@ -477,15 +468,6 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
 
 // Launch when the pass qualifies (complex in/out, no masks, TMA-compatible
 // view); returns false so the caller falls back to the per-tile kernel.
-inline bool tma_store_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SMAT_NO_TMA_STORE");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <class C, int N, int EP, int NB, int CTO = 0>
 inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   using G = TmaGeom<C, N, EP, NB, false, false, CTO>;
@@ -532,7 +514,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
                      blo ? blo : pad ? rlo : 0, pad ? ein : 0, pad, blo ? a.xsi_hi : 0))
     return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
-  const bool ts = tma_store_enabled() && eout > 0 &&
+  const bool ts = eout > 0 &&
                   make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
                                 blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc, blo ? a.ysi_hi : 0);
   if (!ts && blo) return false;  // direct stores are single-level
@@ -553,7 +535,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
       const int grid = int(ntiles < slots ? ntiles : slots);
       auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV, CTO>;
       set_smem(kern, GV::SMEM);
-      if (kPdl<C, N> && pdl_enabled()) {
+      if (kPdl<C, N>) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(grid));
         cfg.blockDim = dim3(unsigned(GV::T));
@@ -588,53 +570,22 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   return ok;
 }
 
-inline int tma_variant() {
-  static int v = -1;
-  if (v < 0) {
-    // 1 (default): radix-32 stages, 3-deep landing ring for complex64 >= 1024
-    // points; 3: radix-16 stages there too.  (Measured and dropped, round 1:
-    // single-buffer two-CTA-per-SM rings (except complex128 1024, above),
-    // the complex128 2048-point spectrum pass with one landing buffer and its
-    // spectrum slice read from L2 so two CTAs fit (2.73 -> 3.49 ms),
-    // 1/2/4-column complex128 tiles,
-    // radix-8 stages for 256..1024 points, and radix-8 stages (16 warps per
-    // SM) for the complex128 512..2048-point passes of C5 (spectrum pass
-    // 2.72 -> 6.63 ms) — all slower.)
-    const char* e = getenv("SMAT_TMA_VARIANT");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
-
-// complex128 1024-point passes: one landing buffer per CTA and two CTAs (16
-// warps) per SM (default; SMAT_TMA_C128_NB1=0 -> two landing buffers, one CTA).
-// These passes are issue-latency bound at 8 warps per SM (ncu: 26% issue
-// utilisation, 0.4 eligible warps per scheduler); the second CTA hides more
-// of it than the lost load lead costs (C5 outer passes 2.34 / 2.00 ->
-// 2.09 / 1.78 ms); the masked twiddle variant C5 uses spills 16 B at 128
-// registers, the spectrum (MID) variants ~300 B, so those keep two buffers.
-inline int tma_c128_nb1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SMAT_TMA_C128_NB1");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
-
+// Variant choice (measured, round 1): radix-32 stages and a
+// 3-deep landing ring for complex64 >= 1024 points; complex128 1024-point
+// passes with one landing buffer and two CTAs (16 warps) per SM except the
+// spectrum passes (at 128 registers their FFT + IFFT spills), which keep two
+// buffers — these passes are issue-latency bound at 8 warps per SM, and the
+// second CTA hides more of it than the lost load lead costs (C5 outer passes
+// 2.34 / 2.00 -> 2.09 / 1.78 ms); radix-16 stages everywhere else.  Tried and
+// dropped: radix-16 / radix-8 stages for the long complex64 passes, radix-8
+// stages for complex128, 1/2/4-column complex128 tiles, single-buffer spectrum
+// passes.
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
   if constexpr (N == 1024 && sizeof(C) == 16) {
-    // (spectrum passes keep two buffers: at 128 registers their FFT + IFFT spills)
-    if (tma_c128_nb1() == 2 || (tma_c128_nb1() == 1 && !a.mid)) return fft_tma_launch_v<C, N, 16, 1>(a, s);
+    if (!a.mid) return fft_tma_launch_v<C, N, 16, 1>(a, s);
   }
-  if constexpr (N >= 1024 && sizeof(C) == 8) {
-    if (tma_variant() != 3) return fft_tma_launch_v<C, N, 32, 3>(a, s);
-  }
-  // short transforms: several CTAs per SM; SMAT_TMA_VARIANT=8 -> radix-8 stages
-  if constexpr (N < 256) {
-    if (tma_variant() == 8) return fft_tma_launch_v<C, N, 8, 0>(a, s);
-  }
+  if constexpr (N >= 1024 && sizeof(C) == 8) return fft_tma_launch_v<C, N, 32, 3>(a, s);
   return fft_tma_launch_v<C, N, 16, 0>(a, s);
 }
 

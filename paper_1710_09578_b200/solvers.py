@@ -25,7 +25,6 @@ and as device tensors for CUDA tensor inputs.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -99,10 +98,13 @@ def _stream():
 
 # how the last solver loop ran: "graph" (captured once, replayed) or "eager"
 last_loop_mode = None
+# solver iterations replay one captured CUDA graph (tests flip this to compare
+# against eager launches)
+_GRAPHS = True
 
 
 def _graphs_enabled() -> bool:
-    return os.environ.get("SMAT_SOLVER_GRAPHS", "1") != "0"
+    return _GRAPHS
 
 
 class _Loop:

@@ -23,10 +23,12 @@ def _run(*args):
 
 
 def test_bench_native_line_contract():
-    d = _run("--workload", "c1", "--steps", "5", "--warmup", "3", "--no-cpu-baseline")
+    d = _run("--workload", "c1", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-per-config")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
-              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "parity"):
         assert k in d, k
+    assert d["parity"]["pass"] and d["parity"]["columns"] == list(range(16))  # C1: every column, bit-exact
+    assert d["config"]["launch"] == "cuda_graph"
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
     assert d["gpu_launches"] > 0 and d["config"]["workload"].startswith("C1")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0

@@ -143,3 +143,52 @@ def test_rowshard_split_lengths():
         rowshard.split_lengths(16, 8)  # 4 x 4 does not split over 8 ranks
     x = np.arange(24).reshape(12, 2)
     assert np.array_equal(rowshard.local_rows(x, 1, 3), x[4:8])
+
+
+def _bench_worker(rank, world, port, q):
+    """One rank of bench.py's multi-GPU path with the device steps replaced by
+    the CPU oracle: the same column slice, the same parity share and the same
+    max-over-ranks / parity reduction the native arm runs over NCCL."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"], os.environ["WORLD_SIZE"] = str(rank), str(world)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from oracle import linop_oracle as orc
+        from paper_1710_09578_b200 import configs
+
+        w = configs.make(2, n=4096)  # C2's seeded draw at a small length, all 64 columns
+        K = w.ncols
+        a, b = sharding.column_slices(K, world)[rank]
+        oop = bench._oracle_op(2, w)
+        y = orc.apply(oop, w.X[:, a:b], 0)
+        z = orc.apply(oop, y, 1)
+        par = bench.rank_parity(2, w, a, b, 8, lambda loc: (y[:, loc], z[:, loc]))
+        ms, parity = bench.reduce_over_ranks(10.0 + rank, par, 2, world, "cpu")
+        q.put((rank, (a, b), ms, parity))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_gloo_world2_bench_shard_parity_reduce():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=170) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+    import bench
+
+    assert [r[1] for r in res] == [(0, 32), (32, 64)]            # strong scaling: the named block split
+    assert all(r[2] == 11.0 for r in res)                          # slowest rank's time on every rank
+    for _, _, _, parity in res:
+        assert parity["pass"] and parity["columns"] == bench.parity_columns(64, 8)
+        assert 0 in parity["columns"] and 63 in parity["columns"]  # first and last column checked
+        assert parity["rel_l2_fwd"] == 0.0
