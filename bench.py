@@ -122,9 +122,9 @@ def _oracle_op(cfg, w):
 
 
 def parity_columns(K: int, want: int) -> list[int]:
-    """At least `want` global columns (all when K <= want), always including
-    the first and the last, the rest evenly spaced."""
-    if K <= want:
+    """At least `want` global columns (all of a block of at most 16 columns),
+    always including the first and the last, the rest evenly spaced."""
+    if K <= max(want, 16):
         return list(range(K))
     cols = {0, K - 1}
     for c in np.linspace(0, K - 1, num=want).astype(int).tolist():

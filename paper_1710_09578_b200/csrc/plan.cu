@@ -341,6 +341,9 @@ struct XformIO {
   // intermediate there, so neither outer pass walks 2 MB-page strides
   bool x_blk = false, y_blk = false;
   int64_t blk_n2b = 0;
+  // Walsh-Hadamard over the first half of the outer pass's rows fused into
+  // pass 1's input (wht_in) / pass 3's output (wht_out): FftArgs::wht_half
+  bool wht_in = false, wht_out = false;
   // fused row selection (single-tile transforms only): see FftArgs::in_map
   const int32_t* in_map = nullptr;
   const int32_t* out_map = nullptr;
@@ -377,6 +380,8 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     return;
   }
   SMAT_CHECK(!io.in_map && !io.out_map, SMAT_UNSUPPORTED, "fused row selection needs a single-tile transform");
+  SMAT_CHECK((!io.wht_in || io.x_blk) && (!io.wht_out || io.y_blk), SMAT_UNSUPPORTED,
+             "fused Walsh-Hadamard stages need the blocked chain layout");
   SMAT_CHECK(Nt <= int64_t(kTileMax) * kTileMax, SMAT_UNSUPPORTED,
              "transform length " + std::to_string(Nt) + " exceeds the two-pass limit 2^24");
   if (!merge_outer(g, io.x, io.y)) {
@@ -441,6 +446,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     }
     a.tw_on = 1; a.tw_inv = 0; a.tw_lo = tw.lo; a.tw_hi = tw.hi; a.tw_lo_bits = tw.lo_bits; a.tw_mask = Nt - 1;
     a.tw_slices = twiddle_slices(c.device, Nt, N2, false, dbl);
+    a.wht_half = io.wht_in ? 1 : 0;
     c.fft(cdt, int(N2), a);
   } else {
     FftArgs a;
@@ -523,6 +529,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.g_div = ic; a.g_mod = N1; a.gout_stride = N1;
       a.n_valid_out = io.y_rows;
       a.inv = 1;
+      a.wht_half = io.wht_out ? 2 : 0;
       if (tw3) {
         // pass 2's inverse twiddle W^-(n1*k2), applied to this pass's input
         a.tw_on = 1; a.tw_pre = 1; a.tw_inv = 1;
@@ -1192,6 +1199,9 @@ struct DFSumNode : Node {
     ma.nw = int(NWa); mb.nw = 64;
     WlrArgs a1, a2;
     a1.r = a2.r = r; a1.K = a2.K = K;
+    // the k2 stages of the Hadamard ride in the Bluestein pass on the blocked
+    // side when it runs on the TMA kernel, else they are a pass of their own
+    const bool fuse_b = tma_wht_ok(int(N2), K);
     if (!adj) {
       // y = DF (H_pad x + U diag(s) V^H x)
       ma.con = true;  // A1: x -> T1 (Ta), partials of V^H x
@@ -1209,27 +1219,38 @@ struct DFSumNode : Node {
       a2.nrows = P; a2.n_out = P;
       a2.w3 = w3;
       c.wlr(mb, a2, "wht_lowrank_b");
-      pass_b(c, Tb.p, Ta.p, false, K, n);
-      XformIO io = df_io(false, Ta, y, n);
+      Blk src = Tb;
+      if (!fuse_b) {
+        pass_b(c, Tb.p, Ta.p, false, K, n);
+        src = Ta;
+      }
+      XformIO io = df_io(false, src, y, n);
       io.x_blk = true;
+      io.wht_in = fuse_b;
       run_xform(c, M, g, io);
     } else {
       // y = (H_pad + V diag(conj s) U^H) DF^H x
       XformIO io = df_io(true, x, Ta, n);
       io.y_blk = true;
       io.y_rows = P;  // rows n..P come out zero (zero-padded post vector)
+      io.wht_out = fuse_b;
       run_xform(c, M, g, io);
-      pass_b(c, Ta.p, Tb.p, true, K, n);
-      mb.con = true;  // A2: T2 (Tb) -> T1 (Ta), partials of U~^H T2
-      a2.in = t2_blocked_in(Tb.p, K);
-      a2.y = Ta.p; a2.yout = t1_by_b(K);
+      Blk t2 = Ta, t1 = Tb;
+      if (!fuse_b) {
+        pass_b(c, Ta.p, Tb.p, true, K, n);
+        t2 = Tb;
+        t1 = Ta;
+      }
+      mb.con = true;  // A2: T2 -> T1, partials of U~^H T2
+      a2.in = t2_blocked_in(t2.p, K);
+      a2.y = t1.p; a2.yout = t1_by_b(K);
       a2.F = lr->Utc->p; a2.n_f = P;
       a2.nrows = P; a2.n_out = P;
       a2.partial = w;
       c.wlr(mb, a2, "wht_lowrank_b");
       c.wlr_fin(w, r, K, sv, true, w3);
-      ma.exp = true;  // A1: T1 (Ta) -> x', + V W''
-      a1.in = t1_by_a_in(Ta.p, K);
+      ma.exp = true;  // A1: T1 -> x', + V W''
+      a1.in = t1_by_a_in(t1.p, K);
       a1.y = y.p; a1.yout = user_rows(y.si);
       a1.F = lr->Ve->p; a1.n_f = n;
       a1.nrows = std::min(P, (n + 63) / 64 * 64); a1.n_out = n;

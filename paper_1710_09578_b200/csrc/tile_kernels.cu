@@ -47,6 +47,15 @@ static bool launch_fft_tma_c128(int N, const FftArgs& a, cudaStream_t s) {
   }
 }
 
+// Whether a complex128 outer four-step pass of length N over `inner` columns
+// runs on the TMA kernel, which can carry a fused half-length Walsh-Hadamard
+// (FftArgs::wht_half): a TMA instantiation exists and whole column tiles.
+bool tma_wht_ok(int N, int64_t inner) {
+  if (N != 256 && N != 512 && N != 1024 && N != 2048) return false;
+  const int ct = N >= 2048 ? 2 : N == 1024 ? 4 : N == 512 ? 8 : 16;  // (TmaGeom::CT, complex128)
+  return inner % ct == 0;
+}
+
 void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
   // persistent TMA-fed variant first (large tiles, complex in and out)
   // (below 256 points only the four-step passes with twiddles / spectra /
@@ -58,6 +67,7 @@ void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
     if (cdt == SMAT_C64 && launch_fft_tma_c64(N, a, s)) return;
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;
   }
+  SMAT_CHECK(!a.wht_half, SMAT_UNSUPPORTED, "fused Walsh-Hadamard stages need the TMA pass");
   if (cdt == SMAT_C64) {
     if (N <= 64) launch_fft_tile_c64_small(N, a, s);
     else launch_fft_tile_c64_large(N, a, s);

@@ -60,6 +60,11 @@ struct FftArgs {
   const int32_t* in_map = nullptr;
   const int32_t* out_map = nullptr;
   int64_t in_rs = 0, out_rs = 0;
+  // Walsh-Hadamard transform over the first N/2 rows of every tile column
+  // fused into the pass (TMA kernel only; the C5 chain's k2 stages of the
+  // padded Hadamard): 1 = on the loaded input, before the masks / pre vector
+  // and the FFT; 2 = on the output, after the post vector, before the store
+  int32_t wht_half = 0;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).
@@ -93,6 +98,7 @@ constexpr int kTileMax = 4096;
 // Launch one FFT tile pass of length N (power of two, 2..4096) in precision
 // `cdt` (SMAT_C64 or SMAT_C128).
 void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s);
+bool tma_wht_ok(int N, int64_t inner);
 // Launch one FWHT tile pass of length N (power of two, 2..4096) on dtype dt.
 void launch_wht_tile(int dt, int N, const WhtArgs& a, cudaStream_t s);
 

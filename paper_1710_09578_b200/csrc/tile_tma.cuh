@@ -78,6 +78,33 @@ template <class C, int N>
 constexpr bool kPdl = sizeof(C) == 8 && N <= 128;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Walsh-Hadamard transform over rows [0, N/2) of every column of a landed /
+// staged tile (natural row order, buf[i * CT + cs]), radix-8 stages with
+// strides 1, 8, 64, ... (stride-1-first); TPC threads per column hold 8
+// elements each (N/2 = 8 TPC).  The load order of each group is rotated by the
+// group index so that the two row groups a memory phase touches differ.
+template <class C, int N, int CT, int TPC, int S = 1>
+__device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
+  constexpr int NH = N / 2;
+  static_assert(NH == 8 * TPC, "8 elements per thread");
+  if constexpr (S < NH) {
+    constexpr int R = NH / S >= 8 ? 8 : NH / S;
+#pragma unroll
+    for (int q = 0; q < 8 / R; ++q) {
+      const int gid = j + q * TPC;
+      const int base = (gid / S) * (S * R) + gid % S;
+      C v[8];
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[k] = buf[(base + k * S) * CT + cs];
+      wht_small<R>(v);
+#pragma unroll
+      for (int k = 0; k < R; ++k) buf[(base + k * S) * CT + cs] = v[k];
+    }
+    __syncthreads();
+    tile_wht_half<C, N, CT, TPC, S * R>(buf, j, cs);
+  }
+}
+
 // launcher-only flags of the TMA pass: the pre (post) vector is stored per
 // tile (pre_gmul / post_gmul) and rides with the tile as a bulk-loaded slice
 enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21 };
@@ -92,7 +119,7 @@ enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21 };
 // pre or post vector arrives as a slice in the stage's side area (like the
 // spectrum of the MID pass).  goff is uniform over a tile (launcher check), so
 // the valid counts are per tile.
-template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK, int CTO>
+template <class C, int N, bool MID, bool TW, int EP, int NB, bool TS, bool MSK, int CTO, int WH = 0>
 __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 0, CTO>::T,
                                   TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 0, CTO>::MINB)
     fft_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
@@ -290,6 +317,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         if (powner && t + gs < ntiles) pval = patch_load(t + gs);
       }
     }
+    if constexpr (WH == 1) tile_wht_half<C, N, CT, TPC>(buf, j, cs);  // (ends with a barrier)
     C a[E];
 #pragma unroll
     for (int u = 0; u < E / R0; ++u)
@@ -444,6 +472,10 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       }
     }
     if constexpr (TS) {
+      if constexpr (WH == 2) {
+        __syncthreads();
+        tile_wht_half<C, N, CT, TPC>(buf, j, cs);
+      }
       fence_proxy_async();  // this thread's tile writes -> visible to the TMA engine
       __syncthreads();
       if (tid == 0) {
@@ -490,12 +522,16 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
     if (v > N) v = N;
     return (v / rlo) * rlo;
   };
-  const int64_t ein = pad ? extent(a.n_valid_in, a.gin_stride) : N;
+  // (a fused Walsh-Hadamard over the first N/2 input rows needs all of them
+  // landed: the row mask applies after it, in registers)
+  const int64_t ein = a.wht_half == 1 ? N / 2 : pad ? extent(a.n_valid_in, a.gin_stride) : N;
   const int64_t eout = trunc ? extent(a.n_valid_out, a.gout_stride) : N;
   if (ein == 0) return false;
+  if (a.wht_half && !(msk && a.tw_on && !a.mid)) return false;
+  if (a.wht_half == 2 && eout > N / 2) return false;
   // rows from ein that only some tiles own (the tile with goff = 0 owns the most)
   int64_t npatch = 0;
-  if (pad) {
+  if (pad && !a.wht_half) {
     int64_t v0 = (a.n_valid_in + a.gin_stride - 1) / a.gin_stride;
     if (v0 > N) v0 = N;
     npatch = v0 - ein;
@@ -510,8 +546,9 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   const int64_t blo = a.i_lo_bits ? (int64_t(1) << a.i_lo_bits) : 0;
   if (blo && (msk || blo > 256 || N / blo > 256 || N % blo)) return false;
   CUtensorMap map, ymap;
+  const bool pin = pad || a.wht_half == 1;
   if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT,
-                     blo ? blo : pad ? rlo : 0, pad ? ein : 0, pad, blo ? a.xsi_hi : 0))
+                     blo ? blo : pin ? rlo : 0, pin ? ein : 0, pin, blo ? a.xsi_hi : 0))
     return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
   const bool ts = eout > 0 &&
@@ -523,9 +560,10 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   if (ntiles <= 0) return true;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag, auto msk_tag) {
+  auto pick = [&](auto ts_tag, auto mid_tag, auto tw_tag, auto msk_tag, auto wh_tag) {
     constexpr bool TSV = decltype(ts_tag)::value, MV = decltype(mid_tag)::value, TV = decltype(tw_tag)::value,
                    KV = decltype(msk_tag)::value;
+    constexpr int WHV = decltype(wh_tag)::value;
     using GV = TmaGeom<C, N, EP, NB, TV, MV ? 1 : KV ? 2 : 0, CTO>;
     if constexpr (GV::SMEM > 232448) {
       return false;  // does not fit one SM: per-tile kernel
@@ -533,7 +571,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
       if (GV::TVSL && !a.tw_slices) return false;  // needs the precomputed twiddle slices
       const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
       const int grid = int(ntiles < slots ? ntiles : slots);
-      auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV, CTO>;
+      auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV, CTO, WHV>;
       set_smem(kern, GV::SMEM);
       if (kPdl<C, N>) {
         cudaLaunchConfig_t cfg = {};
@@ -555,15 +593,26 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   };
   using T_ = std::true_type;
   using F_ = std::false_type;
+  using W0 = std::integral_constant<int, 0>;
   auto pick2 = [&](auto ts_tag) -> bool {
     if (msk) {
-      if (a.tw_on) return pick(ts_tag, F_{}, T_{}, T_{});
-      return pick(ts_tag, F_{}, F_{}, T_{});
+      if (a.tw_on) {
+        // (the fused Walsh-Hadamard variants: complex128 passes of the C5 chain)
+        if constexpr (sizeof(C) == 16 && N >= 256) {
+          if (a.wht_half == 1) return pick(ts_tag, F_{}, T_{}, T_{}, std::integral_constant<int, 1>{});
+          if constexpr (decltype(ts_tag)::value) {
+            if (a.wht_half == 2) return pick(ts_tag, F_{}, T_{}, T_{}, std::integral_constant<int, 2>{});
+          }
+        }
+        if (a.wht_half) return false;
+        return pick(ts_tag, F_{}, T_{}, T_{}, W0{});
+      }
+      return pick(ts_tag, F_{}, F_{}, T_{}, W0{});
     }
-    if (a.mid && a.tw_on) return pick(ts_tag, T_{}, T_{}, F_{});
-    if (a.mid) return pick(ts_tag, T_{}, F_{}, F_{});
-    if (a.tw_on) return pick(ts_tag, F_{}, T_{}, F_{});
-    return pick(ts_tag, F_{}, F_{}, F_{});
+    if (a.mid && a.tw_on) return pick(ts_tag, T_{}, T_{}, F_{}, W0{});
+    if (a.mid) return pick(ts_tag, T_{}, F_{}, F_{}, W0{});
+    if (a.tw_on) return pick(ts_tag, F_{}, T_{}, F_{}, W0{});
+    return pick(ts_tag, F_{}, F_{}, F_{}, W0{});
   };
   const bool ok = ts ? pick2(T_{}) : pick2(F_{});
   if (ok) SMAT_CUDA(cudaGetLastError());
