@@ -1166,6 +1166,46 @@ struct DFSumNode : Node {
     else a.n_valid_out = n;          // forward: rows >= n are not stored
     c.wht(c.dt, int(N2b), a);
   }
+  // Whether the blocked-side Bluestein pass takes the fused k2 Hadamard stages
+  // (TMA kernel): a host-side probe of that pass's launch, cached per
+  // (direction, columns, user-side row stride)
+  mutable std::mutex fuse_mu;
+  mutable std::unordered_map<uint64_t, bool> fuse_memo;
+  bool fuse_ok(const Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g) const {
+    const int64_t K = g.inner;
+    if (!tma_wht_ok(int(N2), K)) return false;
+    const int64_t ld = adj ? x.si : y.si;
+    const uint64_t key = (uint64_t(K) << 33) ^ (uint64_t(ld) << 1) ^ uint64_t(adj);
+    {
+      std::lock_guard<std::mutex> lk(fuse_mu);
+      auto it = fuse_memo.find(key);
+      if (it != fuse_memo.end()) return it->second;
+    }
+    Ctx pc = c;
+    pc.measure = true;
+    pc.probe = true;
+    pc.prof = nullptr;
+    pc.top = pc.peak = 0;
+    Geo gb;
+    gb.inner = K;
+    Blk T = pc.alloc_blk(SMAT_C128, gb, P);
+    bool ok = true;
+    try {
+      XformIO io = adj ? df_io(true, x, T, rows) : df_io(false, T, y, rows);
+      if (adj) {
+        io.y_blk = true; io.y_rows = P; io.wht_out = true;
+      } else {
+        io.x_blk = true; io.wht_in = true;
+      }
+      run_xform(pc, M, g, io);
+    } catch (const Error& e) {
+      if (e.code != SMAT_UNSUPPORTED) throw;
+      ok = false;
+    }
+    std::lock_guard<std::mutex> lk(fuse_mu);
+    fuse_memo[key] = ok;
+    return ok;
+  }
   XformIO df_io(bool adj, const Blk& x, const Blk& y, int64_t n) const {
     XformIO io;
     io.x = x; io.x_rows = n; io.y = y; io.y_rows = n;
@@ -1201,7 +1241,7 @@ struct DFSumNode : Node {
     a1.r = a2.r = r; a1.K = a2.K = K;
     // the k2 stages of the Hadamard ride in the Bluestein pass on the blocked
     // side when it runs on the TMA kernel, else they are a pass of their own
-    const bool fuse_b = tma_wht_ok(int(N2), K);
+    const bool fuse_b = fuse_ok(c, adj, x, y, g);
     if (!adj) {
       // y = DF (H_pad x + U diag(s) V^H x)
       ma.con = true;  // A1: x -> T1 (Ta), partials of V^H x

@@ -46,6 +46,7 @@ struct Ctx {
   char* ws = nullptr;
   size_t ws_size = 0, top = 0, peak = 0;
   bool measure = false;
+  bool probe = false;  // (with measure) ask the launchers whether each pass would run
   int64_t launches = 0;
 
   void* alloc(size_t bytes) {
@@ -96,7 +97,13 @@ struct Ctx {
       if (a.pre || a.post || pad || trunc) lab += "_msk";
     }
     note(lab);
-    if (!measure) launch_fft_tile(cdt, N, a, stream);
+    if (!measure) {
+      launch_fft_tile(cdt, N, a, stream);
+    } else if (probe) {
+      FftArgs q = a;
+      q.probe_only = 1;
+      launch_fft_tile(cdt, N, q, stream);
+    }
   }
   void wht(int d, int N, const WhtArgs& a) {
     ++launches;

@@ -65,6 +65,10 @@ struct FftArgs {
   // padded Hadamard): 1 = on the loaded input, before the masks / pre vector
   // and the FFT; 2 = on the output, after the post vector, before the store
   int32_t wht_half = 0;
+  // probe only: run every check of the launch (TMA view, shared memory) but
+  // launch nothing; launch_fft_tile throws SMAT_UNSUPPORTED where a fused
+  // Walsh-Hadamard pass would not run
+  int32_t probe_only = 0;
 };
 
 // One tiled FWHT pass over the view (stride-1-first stage order).

@@ -569,6 +569,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
       return false;  // does not fit one SM: per-tile kernel
     } else {
       if (GV::TVSL && !a.tw_slices) return false;  // needs the precomputed twiddle slices
+      if (a.probe_only) return true;
       const int64_t slots = int64_t(num_sms(dev)) * GV::MINB;
       const int grid = int(ntiles < slots ? ntiles : slots);
       auto kern = fft_tma_kernel<C, N, MV, TV, EP, NB, TSV, KV, CTO, WHV>;
