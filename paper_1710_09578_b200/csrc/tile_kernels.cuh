@@ -65,6 +65,12 @@ struct FftArgs {
   // padded Hadamard): 1 = on the loaded input, before the masks / pre vector
   // and the FFT; 2 = on the output, after the post vector, before the store
   int32_t wht_half = 0;
+  // column-grouped side (the complex128 four-step intermediate of the
+  // convolution passes, run_xform): when x_cg (y_cg) > 0, column c of a batch
+  // sits at (c / cg) * cg_stride + c % cg, and the o2 index (stride xs2 == cg)
+  // with c % cg forms one contiguous run — TMA kernel only, cg == its column tile
+  int32_t x_cg = 0, y_cg = 0;
+  int64_t x_cg_stride = 0, y_cg_stride = 0;
   // probe only: run every check of the launch (TMA view, shared memory) but
   // launch nothing; launch_fft_tile throws SMAT_UNSUPPORTED where a fused
   // Walsh-Hadamard pass would not run

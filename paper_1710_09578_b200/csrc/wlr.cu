@@ -47,30 +47,48 @@ namespace smat {
 namespace {
 
 constexpr int TR = 64;              // unit rows
-constexpr int KC = 64;              // columns per chunk
+constexpr int KC = 32;              // columns per unit (and per column chunk)
 constexpr int RK = 32;              // padded rank
 // shared-memory row pitches (bytes).  The tensor-core fragments read 16-byte
 // entries of rows lane%4 (contraction: data and factor rows) or lane/4
 // (expansion: factor rows); a pitch of 2 (mod 8) or 4 (mod 8) 16-byte units
 // puts those rows on distinct bank groups.  The data tile is a tensor-map
-// box of KCB = 66 columns (the two extra columns are never used), so it lands
+// box of KCB = 34 columns (the two extra columns are never used), so it lands
 // with that pitch; the factor rows are stored padded in global memory.
 constexpr int KCB = KC + 2;
-constexpr int DP = KCB * 16;        // 1056
+constexpr int DP = KCB * 16;        // 544
 constexpr int FPC = (RK + 2) * 16;  // 544, contraction
 constexpr int FPE = (RK + 4) * 16;  // 576, expansion
-constexpr int NTHR = 256;
-// ring depth per CTA and CTAs per SM: one single-stage CTA per ~half SM, so
-// that while one CTA waits for its tile or stores, the other multiplies
-constexpr int NST = 1;
-constexpr int MINB = 2;
+// One CTA per SM, two consumer groups of four warps (8 columns each) taking
+// alternate units, two rings of shared-memory stages — unit data tiles (4
+// deep) and unit factor rows (2 deep).  The thread that releases a stage
+// issues its refill (the unit NSD / NSF further on), so the data ring runs two
+// units ahead of the consumers.  The groups' tensor-core phases (contraction
+// / expansion) are serialised in unit order through two mbarriers, so one
+// group multiplies while the other transforms and stores (left to themselves
+// the groups phase-lock: both multiply at half rate, then both stream); the
+// factor rows are needed only in that phase, hence their shorter ring.  Eight
+// warps, two per SM sub-partition, leave each thread up to 255 registers
+// (a ninth, producer warp would cap them at 168 and spill the expansion).
+// (The single-stage two-CTA layout measured load + tensor work + transform +
+// store in series: 1.39 ms per C5 pass, of which 0.65 ms tensor work.)
+constexpr int GTHR = 128;                // threads per consumer group
+constexpr int NGRP = 2;                  // consumer groups
+constexpr int NTHR = NGRP * GTHR;
+constexpr int NSD = 4;                   // data ring stages
+constexpr int NSF = 2;                   // factor ring stages
+// (timing experiments only, tools/exp_build.py: skip phases; results wrong)
+#ifndef WLR_SKIP
+#define WLR_SKIP 0
+#endif
 
 template <bool EXP>
 struct WlrGeom {
   static constexpr int FP = EXP ? FPE : FPC;
   static constexpr int DATA = TR * DP;
-  static constexpr int STAGE = DATA + TR * FP;
-  static constexpr int SMEM = NST * STAGE + 64;
+  static constexpr int FACT = TR * FP;
+  static constexpr int NBAR = NSD + NSF + NGRP;
+  static constexpr int SMEM = NSD * DATA + NSF * FACT + NBAR * 8;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -131,7 +149,7 @@ template <int R, int S, int NW>
 __device__ __forceinline__ void wht_stage(unsigned char* dbuf, int c, int p) {
   constexpr int NG = TR / R;
 #pragma unroll
-  for (int j = p; j < NG; j += NTHR / KC) {
+  for (int j = p; j < NG; j += GTHR / KC) {
     const int b0 = S == 1 ? R * j : NW * (j / 8) + j % 8;
     double2 v[8];
 #pragma unroll
@@ -142,19 +160,35 @@ __device__ __forceinline__ void wht_stage(unsigned char* dbuf, int c, int p) {
   }
 }
 
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier of one consumer group (ids 1, 2; 0 is __syncthreads)
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GTHR) : "memory");
+}
+
 template <int NW, bool CON, bool EXP, bool IN, bool OUT>
-__global__ void __launch_bounds__(NTHR, MINB)
+__global__ void __launch_bounds__(NTHR, 1)
     wlr_kernel(const __grid_constant__ CUtensorMap xmap, const WlrArgs a, const int nchunks, const int nunits) {
   using G = WlrGeom<EXP>;
   constexpr int FP = G::FP;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * G::STAGE);
+  unsigned char* dring = smem;                  // data tiles
+  unsigned char* fring = smem + NSD * G::DATA;  // factor rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(fring + NSF * G::FACT);
+  uint64_t* ffull = full + NSD;
+  uint64_t* mma_done = ffull + NSF;  // per group: its tensor phase of a unit is issued
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / 4;  // consumer group 0 / 1
   const int ch = int(blockIdx.x) % nchunks;
   const int64_t c0 = int64_t(ch) * KC;
   const int kcv = int(min(int64_t(KC), a.K - c0));  // valid columns of this CTA's chunk
   const int r = int(a.r);
   const int gs = int(gridDim.x);
+  // this CTA's units: blockIdx.x + i * gs, i < nloc (gs is a multiple of
+  // nchunks, so every unit of the CTA is in column chunk ch)
+  const int nloc = int(blockIdx.x) < nunits ? (nunits - 1 - int(blockIdx.x)) / gs + 1 : 0;
   double2* Y = reinterpret_cast<double2*>(a.y);
   const double2* F = reinterpret_cast<const double2*>(a.F);
   const int lgw = a.in.kind == WLR_IN_ROWS ? 0 : ilog2_dev(int(a.in.nwa));
@@ -163,39 +197,72 @@ __global__ void __launch_bounds__(NTHR, MINB)
     const int64_t v = lim - g0;
     return v <= 0 ? 0 : v >= TR ? TR : int(v);
   };
-  // one thread: the unit's input box (one tensor-map copy) and its factor
-  // rows (one bulk copy of the padded rows) into stage s
-  auto issue = [&](int u, int s) {
-    const int64_t g0 = int64_t(u / nchunks) * TR;
-    unsigned char* dbuf = smem + s * G::STAGE;
-    unsigned char* fbuf = dbuf + G::DATA;
-    const int rf = rows_valid(min(a.n_f, a.nrows), g0);
-    const uint32_t fbytes = uint32_t(rf) * FP;
-    mbar_arrive_expect_tx(&bars[s], (IN ? uint32_t(G::DATA) : 0u) + fbytes);
-    if constexpr (IN) {
-      const int cw = int(2 * c0);
-      if (a.in.kind == WLR_IN_ROWS) {
-        tma_load_2d(dbuf, &xmap, &bars[s], cw, int(g0));
-      } else if (a.in.kind == WLR_IN_T1A) {
-        const int T0 = int(g0 >> lgw);
-        tma_load_4d(dbuf, &xmap, &bars[s], cw, 0, T0 & 63, T0 >> 6);
-      } else {
-        const int Tp = int(g0 >> 6);
-        tma_load_5d(dbuf, &xmap, &bars[s], cw, 0, 0, Tp & int(a.in.nwa - 1), Tp >> lgw);
-      }
-    }
-    if (rf) bulk_load(fbuf, F + g0 * (FP / 16), fbytes, &bars[s]);
-  };
-
   if (tid == 0) {
-    if constexpr (IN) tma_prefetch_desc(&xmap);
-    for (int st = 0; st < NST; ++st) mbar_init(&bars[st], 1);
+    for (int st = 0; st < NSD; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < NSF; ++st) mbar_init(&ffull[st], 1);
+    for (int g = 0; g < NGRP; ++g) mbar_init(&mma_done[g], 1);
     fence_barrier_init();
-    for (int st = 0; st < NST; ++st)
-      if (int(blockIdx.x) + st * gs < nunits) issue(blockIdx.x + st * gs, st);
   }
   __syncthreads();
 
+  // unit i's input box (one tensor-map copy) into data stage i % NSD, its
+  // factor rows (one bulk copy of the padded rows) into factor stage i % NSF
+  auto issue_data = [&](int i) {
+    if constexpr (IN) {
+      const int u = int(blockIdx.x) + i * gs;
+      const int64_t g0 = int64_t(u / nchunks) * TR;
+      const int s = i % NSD;
+      unsigned char* dbuf = dring + s * G::DATA;
+      mbar_arrive_expect_tx(&full[s], uint32_t(G::DATA));
+      const int cw = int(2 * c0);
+      if (a.in.kind == WLR_IN_ROWS) {
+        tma_load_2d(dbuf, &xmap, &full[s], cw, int(g0));
+      } else if (a.in.kind == WLR_IN_T1A) {
+        const int T0 = int(g0 >> lgw);
+        tma_load_4d(dbuf, &xmap, &full[s], cw, 0, T0 & 63, T0 >> 6);
+      } else {
+        const int Tp = int(g0 >> 6);
+        tma_load_5d(dbuf, &xmap, &full[s], cw, 0, 0, Tp & int(a.in.nwa - 1), Tp >> lgw);
+      }
+    }
+  };
+  auto issue_factor = [&](int i) {
+    const int u = int(blockIdx.x) + i * gs;
+    const int64_t g0 = int64_t(u / nchunks) * TR;
+    const int sf = i % NSF;
+    const int rf = rows_valid(min(a.n_f, a.nrows), g0);
+    const uint32_t fbytes = uint32_t(rf) * FP;
+    mbar_arrive_expect_tx(&ffull[sf], fbytes);
+    if (rf) bulk_load(fring + sf * G::FACT, F + g0 * (FP / 16), fbytes, &ffull[sf]);
+  };
+  if (tid == 0) {
+    if constexpr (IN) tma_prefetch_desc(&xmap);
+    for (int i = 0; i < NSD && i < nloc; ++i) issue_data(i);
+    for (int i = 0; i < NSF && i < nloc; ++i) issue_factor(i);
+  }
+
+  // ---- consumer group grp: units i = grp, grp + 2, ...
+  const int gt = tid - grp * GTHR, gw = gt >> 5;  // thread / warp within the group
+  // tensor phase of unit i (the group's k-th, i = 2k + grp) starts after unit
+  // i - 1's: group 0 waits for group 1's (k-1)-th, group 1 for group 0's k-th
+  // (the acquire also waits for the unit's factor rows and zeroes the rows
+  // past the factor's end; the release frees their stage)
+  auto mma_acquire = [&](int i, unsigned char* fbuf, int rf) {
+    if (i > 0) mbar_wait(&mma_done[1 - grp], uint32_t(((i - 1) / NGRP) & 1));
+    mbar_wait(&ffull[i % NSF], uint32_t((i / NSF) & 1));
+    if (rf < TR) {
+      for (int e = rf * (FP / 16) + gt; e < TR * (FP / 16); e += GTHR) st2(fbuf + e * 16, make_double2(0.0, 0.0));
+      group_sync(grp);
+    }
+  };
+  auto mma_release = [&](int i) {
+    fence_proxy_async();
+    group_sync(grp);
+    if (gt == 0) {
+      mbar_arrive1(&mma_done[grp]);
+      if (i + NSF < nloc) issue_factor(i + NSF);  // (factor stage free)
+    }
+  };
   // contraction partials: q-tile mt (rows 8mt.. of W), product p (Gauss), pair
   double acc[4][3][2];
 #pragma unroll
@@ -203,10 +270,10 @@ __global__ void __launch_bounds__(NTHR, MINB)
 #pragma unroll
     for (int p = 0; p < 3; ++p) acc[i][p][0] = acc[i][p][1] = 0.0;
   // expansion: this lane's W' fragments for every k-step (q = 4ks + lane%4,
-  // column 8*warp + lane/4 of the chunk)
+  // column 8*gw + lane/4 of the chunk)
   double wb[EXP ? 8 : 1][3];
   if constexpr (EXP) {
-    const int64_t col = c0 + 8 * warp + (lane >> 2);
+    const int64_t col = c0 + 8 * gw + (lane >> 2);
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       const int q = 4 * ks + (lane & 3);
@@ -216,110 +283,141 @@ __global__ void __launch_bounds__(NTHR, MINB)
     }
   }
 
-  for (int u = blockIdx.x, it = 0; u < nunits; u += gs, ++it) {
-    const int s = it % NST;
-    unsigned char* dbuf = smem + s * G::STAGE;
-    unsigned char* fbuf = dbuf + G::DATA;
+  for (int i = grp; i < nloc; i += NGRP) {
+    const int s = i % NSD, sf = i % NSF;
+    const int u = int(blockIdx.x) + i * gs;
+    unsigned char* dbuf = dring + s * G::DATA;
+    unsigned char* fbuf = fring + sf * G::FACT;
     const int64_t g0 = int64_t(u / nchunks) * TR;
-    mbar_wait(&bars[s], uint32_t((it / NST) & 1));
-    // zero what the copies did not fill: the whole tile without an input,
-    // factor rows past the factor's end
-    const int rf = rows_valid(min(a.n_f, a.nrows), g0);
-    if (!IN || rf < TR) {
-      if (!IN) {
-        for (int e = tid; e < TR * KCB; e += NTHR) st2(dbuf + e * 16, make_double2(0.0, 0.0));
-      }
-      for (int e = rf * (FP / 16) + tid; e < TR * (FP / 16); e += NTHR) st2(fbuf + e * 16, make_double2(0.0, 0.0));
-      __syncthreads();
+    if constexpr (IN) {
+      mbar_wait(&full[s], uint32_t((i / NSD) & 1));
+    } else {
+      // without an input the tile starts as zeros (output = F W' only)
+      for (int e = gt; e < TR * KCB; e += GTHR) st2(dbuf + e * 16, make_double2(0.0, 0.0));
+      group_sync(grp);
     }
+    const int rf = rows_valid(min(a.n_f, a.nrows), g0);
 
-    if constexpr (CON) {
+    if constexpr (CON) mma_acquire(i, fbuf, rf);
+    if constexpr (CON && !(WLR_SKIP & 1)) {
       // W_part[q][c] += sum_t conj(F[t][q]) X[t][c]  (warp: 8 columns, all 32 q)
       //   T1 = Fr Xr, T2 = Fi Xi, T3 = (Fr - Fi)(Xr + Xi):  Re = T1 + T2, Im = T3 - T1 + T2
-      const int cb = (8 * warp + (lane >> 2)) * 16;
-#pragma unroll 2
+      // (operands of k-step ks + 1 are loaded and their Gauss sums formed
+      // while ks multiplies: no load or add sits between dependent MMAs)
+      const int cb = (8 * gw + (lane >> 2)) * 16;
+      const unsigned char* xr0 = dbuf + (lane & 3) * DP + cb;
+      const unsigned char* fr0 = fbuf + (lane & 3) * FP + (lane >> 2) * 16;
+      double2 xv = ld2(xr0), fv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) fv[mt] = ld2(fr0 + mt * 128);
+#pragma unroll
       for (int ks = 0; ks < TR / 4; ++ks) {
-        const int row = 4 * ks + (lane & 3);
-        const double2 xv = ld2(dbuf + row * DP + cb);
         const double bs = xv.x + xv.y;
+        double fd[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) fd[mt] = fv[mt].x - fv[mt].y;
+        const double2 xc = xv;
+        double2 fc[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) fc[mt] = fv[mt];
+        if (ks + 1 < TR / 4) {
+          xv = ld2(xr0 + (ks + 1) * 4 * DP);
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) fv[mt] = ld2(fr0 + (ks + 1) * 4 * FP + mt * 128);
+        }
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
-          const double2 fv = ld2(fbuf + row * FP + (8 * mt + (lane >> 2)) * 16);
-          dmma(acc[mt][0], fv.x, xv.x);
-          dmma(acc[mt][1], fv.y, xv.y);
-          dmma(acc[mt][2], fv.x - fv.y, bs);
+          dmma(acc[mt][0], fc[mt].x, xc.x);
+          dmma(acc[mt][1], fc[mt].y, xc.y);
+          dmma(acc[mt][2], fd[mt], bs);
         }
       }
     }
-    if constexpr (NW > 1) {
-      if constexpr (CON) __syncthreads();  // contraction reads of the untransformed rows are done
-      const int c = tid % KC, p = tid / KC;
+    // (the release's group barrier also ends the contraction's reads of the
+    // untransformed rows)
+    if constexpr (CON) mma_release(i);
+    if constexpr (NW > 1 && !(WLR_SKIP & 2)) {
+      const int c = gt % KC, p = gt / KC;
       wht_stage<(NW < 8 ? NW : 8), 1, NW>(dbuf, c, p);  // strides 1, 2, 4
-      __syncthreads();
+      group_sync(grp);
       if constexpr (NW > 8) {
         wht_stage<NW / 8, 8, NW>(dbuf, c, p);  // strides 8 .. NW/2
-        __syncthreads();
+        group_sync(grp);
       }
     }
-    if constexpr (EXP) {
-      // Y[t][c] += sum_q G[t][q] W'[q][c]  (warp: 8 columns; rows in two halves)
+    if constexpr (EXP) mma_acquire(i, fbuf, rf);
+    if constexpr (EXP && !(WLR_SKIP & 4)) {
+      // Y[t][c] += sum_q G[t][q] W'[q][c]  (warp: 8 columns; rows in quarters)
       //   T1 = Gr Wr, T2 = Gi Wi, T3 = (Gr + Gi)(Wr + Wi):  Re = T1 - T2, Im = T3 - T1 - T2
 #pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        double e[4][3][2];
+      for (int qr = 0; qr < 4; ++qr) {
+        double e[2][3][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-          for (int p = 0; p < 3; ++p) e[i][p][0] = e[i][p][1] = 0.0;
+          for (int p = 0; p < 3; ++p) e[i2][p][0] = e[i2][p][1] = 0.0;
+        // (k-step ks + 1's factor entries and sums are formed while ks multiplies)
+        const unsigned char* g0p = fbuf + (16 * qr + (lane >> 2)) * FP + (lane & 3) * 16;
+        double2 gv[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) gv[mt] = ld2(g0p + mt * 8 * FP);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          const int q = 4 * ks + (lane & 3);
+          double2 gc[2];
+          double gs2[2];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int row = 32 * half + 8 * mt + (lane >> 2);
-            const double2 gv = ld2(fbuf + row * FP + q * 16);
-            dmma(e[mt][0], gv.x, wb[ks][0]);
-            dmma(e[mt][1], gv.y, wb[ks][1]);
-            dmma(e[mt][2], gv.x + gv.y, wb[ks][2]);
+          for (int mt = 0; mt < 2; ++mt) {
+            gc[mt] = gv[mt];
+            gs2[mt] = gv[mt].x + gv[mt].y;
+          }
+          if (ks + 1 < 8) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) gv[mt] = ld2(g0p + mt * 8 * FP + (ks + 1) * 64);
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            dmma(e[mt][0], gc[mt].x, wb[ks][0]);
+            dmma(e[mt][1], gc[mt].y, wb[ks][1]);
+            dmma(e[mt][2], gs2[mt], wb[ks][2]);
           }
         }
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const int row = 32 * half + 8 * mt + (lane >> 2);
+        for (int mt = 0; mt < 2; ++mt) {
+          const int row = 16 * qr + 8 * mt + (lane >> 2);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            unsigned char* pp = dbuf + row * DP + (8 * warp + 2 * (lane & 3) + j) * 16;
+            unsigned char* pp = dbuf + row * DP + (8 * gw + 2 * (lane & 3) + j) * 16;
             const double2 v = ld2(pp);
             st2(pp, make_double2(v.x + e[mt][0][j] - e[mt][1][j], v.y + e[mt][2][j] - e[mt][0][j] - e[mt][1][j]));
           }
         }
       }
-      __syncthreads();
     }
-    if constexpr (OUT) {
-      // thread: column c, rows t = tid / 64 + 4 j (coalesced 1 KB rows)
+    if constexpr (EXP) mma_release(i);  // (also: the expanded rows are written)
+    if constexpr (OUT && !(WLR_SKIP & 8)) {
+      // thread: column c, rows t = gt / 32 + 4 j (coalesced 512-byte rows)
       const int rout = rows_valid(min(a.n_out, a.nrows), g0);
-      const int c = tid % KC;
+      const int c = gt % KC;
       if (c < kcv) {
-        for (int t = tid / KC; t < rout; t += NTHR / KC)
+        for (int t = gt / KC; t < rout; t += GTHR / KC)
           Y[wlr_phys<NW>(a.yout, g0 + t) * a.yout.ld + c0 + c] = ld2(dbuf + t * DP + c * 16);
       }
     }
-    __syncthreads();  // stage s is free
-    if (tid == 0 && u + NST * gs < nunits) {
-      fence_proxy_async();
-      issue(u + NST * gs, s);
-    }
+    // stage s is free: order this group's generic-proxy accesses before the
+    // producer's next asynchronous copy into it, then release it
+    fence_proxy_async();
+    group_sync(grp);
+    if (IN && gt == 0 && i + NSD < nloc) issue_data(i + NSD);  // (data stage free)
   }
 
   if constexpr (CON) {
-    double2* P = reinterpret_cast<double2*>(a.partial) + int64_t(blockIdx.x) * RK * KC;
+    double2* P = reinterpret_cast<double2*>(a.partial) + (int64_t(blockIdx.x) * NGRP + grp) * RK * KC;
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       const int q = 8 * mt + (lane >> 2);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int c = 8 * warp + 2 * (lane & 3) + j;
+        const int c = 8 * gw + 2 * (lane & 3) + j;
         P[q * KC + c] = make_double2(acc[mt][0][j] + acc[mt][1][j], acc[mt][2][j] - acc[mt][0][j] + acc[mt][1][j]);
       }
     }
@@ -335,11 +433,12 @@ __global__ void wlr_finalize_kernel(const double2* partial, int grid, int nchunk
     const int ch = int(c / KC), cc = int(c % KC);
     double2 sum = make_double2(0.0, 0.0);
     if (q < r) {
-      for (int b = ch; b < grid; b += nchunks) {  // fixed order: deterministic
-        const double2 v = partial[(int64_t(b) * RK + q) * KC + cc];
-        sum.x += v.x;
-        sum.y += v.y;
-      }
+      for (int b = ch; b < grid; b += nchunks)  // fixed order: deterministic
+        for (int g = 0; g < NGRP; ++g) {
+          const double2 v = partial[((int64_t(b) * NGRP + g) * RK + q) * KC + cc];
+          sum.x += v.x;
+          sum.y += v.y;
+        }
       if (s) {
         double2 sv = s[q];
         if (s_conj) sv.y = -sv.y;
@@ -426,11 +525,11 @@ void wlr_pad_factor(const void* src, void* dst, int64_t rows, int64_t r, bool ex
 
 int wlr_grid(int device, int64_t K) {
   const int nchunks = int((K + KC - 1) / KC);
-  const int per = MINB * num_sms(device) / nchunks;
+  const int per = num_sms(device) / nchunks;
   return nchunks * (per > 0 ? per : 1);
 }
 
-size_t wlr_partial_bytes(int device, int64_t K) { return size_t(wlr_grid(device, K)) * RK * KC * 16; }
+size_t wlr_partial_bytes(int device, int64_t K) { return size_t(wlr_grid(device, K)) * NGRP * RK * KC * 16; }
 
 int launch_wlr(const WlrMode& m, const WlrArgs& a, int device, cudaStream_t s, bool dry) {
   SMAT_CHECK(a.r >= 1 && a.r <= RK, SMAT_UNSUPPORTED, "wlr: rank must be 1..32");
