@@ -222,8 +222,8 @@ _REF = {}
 
 def _ref_module():
     """The unmodified reference package: baseline/_ref (pip --target install of
-    /root/reference, travels with the repo), else /root/reference/pkg/src."""
-    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+    /root/reference, git-ignored, travels to the GPU box with the repo)."""
+    for p in (ROOT / "baseline" / "_ref",):
         if (p / "linopkit" / "__init__.py").exists():
             sys.path.insert(0, str(p))
             try:
