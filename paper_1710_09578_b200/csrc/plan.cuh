@@ -48,6 +48,11 @@ struct Ctx {
   bool measure = false;
   bool probe = false;  // (with measure) ask the launchers whether each pass would run
   int64_t launches = 0;
+  // fused 8-point Walsh-Hadamard for the next single-tile transform
+  // (KronNode's Hadamard x FFT passes, FftArgs::wht_grp); run_xform consumes it
+  int wgrp = 0;
+  int64_t wg_xs = 0, wg_ys = 0;
+  bool wg_used = false;
 
   void* alloc(size_t bytes) {
     size_t off = (top + 255) & ~size_t(255);

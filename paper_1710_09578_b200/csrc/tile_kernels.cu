@@ -62,13 +62,14 @@ void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
   // masks: the plain short passes run at HBM speed on the per-tile kernel)
   const bool pad = (a.g_mod - 1) + (N - 1) * a.gin_stride >= a.n_valid_in;
   const bool trunc = (a.g_mod - 1) + (N - 1) * a.gout_stride >= a.n_valid_out;
-  const bool extras = a.mid || a.tw_on || a.pre || a.post || pad || trunc;
+  const bool extras = a.mid || a.tw_on || a.pre || a.post || pad || trunc || a.wht_grp;
   if (N >= 256 || (N >= 64 && extras)) {
     if (cdt == SMAT_C64 && launch_fft_tma_c64(N, a, s)) return;
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;
   }
   SMAT_CHECK(!a.wht_half, SMAT_UNSUPPORTED, "fused Walsh-Hadamard stages need the TMA pass");
   SMAT_CHECK(!a.x_cg && !a.y_cg, SMAT_UNSUPPORTED, "column-grouped views need the TMA pass");
+  SMAT_CHECK(!a.wht_grp, SMAT_UNSUPPORTED, "fused Kron Walsh-Hadamard needs the TMA pass");
   if (a.probe_only) return;
   if (cdt == SMAT_C64) {
     if (N <= 64) launch_fft_tile_c64_small(N, a, s);

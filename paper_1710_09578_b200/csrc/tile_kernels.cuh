@@ -71,6 +71,13 @@ struct FftArgs {
   // with c % cg forms one contiguous run — TMA kernel only, cg == its column tile
   int32_t x_cg = 0, y_cg = 0;
   int64_t x_cg_stride = 0, y_cg_stride = 0;
+  // fused 8-point Walsh-Hadamard across a batch index (Kron(Hadamard, ...),
+  // KronNode): the batch's inner index is virtual, v = (column group of 4,
+  // hh, column % 4) with hh (element strides wg_xs / wg_ys) the Hadamard
+  // index; a tile is 4 columns x 8 hh (TMA kernel only, 32-column tiles) and
+  // the transform runs across lane bits 2-4 on the loaded input
+  int32_t wht_grp = 0;
+  int64_t wg_xs = 0, wg_ys = 0;
   // probe only: run every check of the launch (TMA view, shared memory) but
   // launch nothing; launch_fft_tile throws SMAT_UNSUPPORTED where a fused
   // Walsh-Hadamard pass would not run

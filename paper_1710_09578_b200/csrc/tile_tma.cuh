@@ -110,9 +110,31 @@ __device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
   }
 }
 
+// 8-point Walsh-Hadamard over the Kron Hadamard index hh of a tile whose
+// column cs = hh * CG + col (CT = 8 CG columns; FftArgs::wht_grp): the hh bits
+// that are lane bits (cs bits < 5) run as butterfly stages over warp
+// shuffles — no shared memory, no barrier; for CT = 64 the top bit (cs bit 5)
+// is folded into the stage-0 load instead (fused_kron_load).
+template <class C, int E, int CT>
+__device__ __forceinline__ void wht_lanes8(C* a) {
+  constexpr int CG = CT / 8;
+  const int lane = int(threadIdx.x) & 31;
+#pragma unroll
+  for (int m = CG; m <= 16; m <<= 1) {
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const auto ox = __shfl_xor_sync(0xffffffffu, a[e].x, m);
+      const auto oy = __shfl_xor_sync(0xffffffffu, a[e].y, m);
+      a[e].x = hi ? ox - a[e].x : a[e].x + ox;
+      a[e].y = hi ? oy - a[e].y : a[e].y + oy;
+    }
+  }
+}
+
 // launcher-only flags of the TMA pass: the pre (post) vector is stored per
 // tile (pre_gmul / post_gmul) and rides with the tile as a bulk-loaded slice
-enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21, F_TSWZ = 1u << 24 };
+enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21, F_TSWZ = 1u << 24, F_WGRP = 1u << 25 };
 
 // MSK: the masked variant for the Bluestein / pruned-embedding passes — zero
 // padding of input rows (g = goff + i*gin_stride >= n_valid_in), truncation of
@@ -180,6 +202,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     // (a column-grouped side: the tile's (o2, column group) run, see FftArgs::x_cg)
     if (f & F_XCG)
       tma_load_5d(stage_buf(s), &xmap, &bars[s], int(o2 * CT * (sizeof(C) / 8)), 0, 0, int(c0 / CT), int(o1));
+    else if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
+      tma_load_5d(stage_buf(s), &xmap, &bars[s], int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
     else
       tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
     if (sb || TVSL) {
@@ -343,7 +367,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       for (int r = 0; r < R0; ++r) {
         // (rows past the tile's valid count were not loaded: zero padding)
         const int i = j + u * TPC + r * (N / R0);
-        a[u * R0 + r] = (!MSK || i < vin) ? buf[i * CT + cs] : C{};
+        if constexpr (WH == 3 && CT == 64) {
+          // (hh's top bit, cs bit 5: own and partner column of the landed row)
+          const C o = buf[i * CT + cs], q = buf[i * CT + (cs ^ 32)];
+          a[u * R0 + r] = (cs & 32) ? q - o : o + q;
+        } else {
+          a[u * R0 + r] = (!MSK || i < vin) ? buf[i * CT + cs] : C{};
+        }
       }
     if ((MSK && p.pre) || twpre) {
       // conj_x, the pre vector, the input twiddle, then the inverse conjugation
@@ -384,6 +414,10 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     } else if (sx < R(0)) {
 #pragma unroll
       for (int e = 0; e < E; ++e) a[e].y = -a[e].y;
+    }
+    if constexpr (WH == 3) {
+      static_assert(CT == 32 || CT == 64, "the fused Kron Walsh-Hadamard needs 32- or 64-column tiles");
+      if constexpr (!(FFT_SKIP & 4)) wht_lanes8<C, E, CT>(a);
     }
     if constexpr (!(FFT_SKIP & 1)) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
     if constexpr (MID) {
@@ -501,6 +535,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         decode_batch(tile_b0(t), p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, q1, q2, c0);
         if (f & F_YCG)
           tma_store_5d(&ymap, buf, int(q2 * CT * (sizeof(C) / 8)), 0, 0, int(c0 / CT), int(q1));
+        else if (f & F_WGRP)
+          tma_store_5d(&ymap, buf, int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
         else
           tma_store_5d(&ymap, buf, int(c0 * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
         bulk_commit();
@@ -559,6 +595,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
     if (npatch * G::CT > G::T) return false;
   }
   FftDev d = d0;
+  if (a.wht_grp) d.flags |= F_WGRP;
   if (a.x_cg) d.flags |= F_XCG;
   if (a.y_cg) d.flags |= F_YCG;
   if (a.x_cg || a.y_cg) d.flags |= F_TSWZ;
@@ -570,12 +607,40 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   const int64_t blo = a.i_lo_bits ? (int64_t(1) << a.i_lo_bits) : 0;
   if (blo && (msk || blo > 256 || N / blo > 256 || N % blo)) return false;
   CUtensorMap map, ymap;
+  if (a.wht_grp) {
+    // fused Kron Walsh-Hadamard: both sides as {columns, hh, rows, o2, o1}
+    // with 4-column x 8-hh boxes (single-dimension rows: N <= 256)
+    if ((G::CT != 32 && G::CT != 64) || N > 256 || msk || a.tw_on || blo || a.x_cg || a.y_cg || a.wht_half ||
+        a.inner % G::CT || a.x_real || a.y_real)
+      return false;
+    const int64_t ic = a.inner / 8;
+    auto gmap = [&](CUtensorMap* m, const void* ptr, int64_t s1, int64_t s2, int64_t si, int64_t sw) {
+      auto fn = encode_fn();
+      if (!fn || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+      const int64_t w = int64_t(sizeof(C) / 8), e = int64_t(sizeof(C));
+      const int64_t n1v = a.nb / (a.n2 * a.inner);
+      cuuint64_t dims[5] = {cuuint64_t(ic * w), 8, cuuint64_t(N), cuuint64_t(a.n2), cuuint64_t(n1v)};
+      cuuint64_t strides[4] = {cuuint64_t(sw * e), cuuint64_t(si * e), cuuint64_t(s2 * e), cuuint64_t(s1 * e)};
+      for (int k = 0; k < 4; ++k) {
+        if (dims[k + 1] == 1) strides[k] = 16;
+        if (strides[k] % 16 || strides[k] >= (cuuint64_t(1) << 40)) return false;
+      }
+      cuuint32_t box[5] = {cuuint32_t(G::CT / 8 * w), 8, cuuint32_t(N), 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+      return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<void*>(ptr), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (!gmap(&map, a.x, a.xs1, a.xs2, a.xsi, a.wg_xs) || !gmap(&ymap, a.y, a.ys1, a.ys2, a.ysi, a.wg_ys))
+      return false;
+  }
   const bool pin = pad || a.wht_half == 1;
   // column-grouped sides: one column tile per group, the o2 rows and the
   // group's columns contiguous, no masked rows (every access is a TMA box)
   if (a.x_cg && (a.x_cg != G::CT || a.xs2 != a.x_cg || blo || pad || a.inner % a.x_cg)) return false;
   if (a.y_cg && (a.y_cg != G::CT || a.ys2 != a.y_cg || blo || trunc || a.inner % a.y_cg)) return false;
-  if (a.x_cg ? !make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.inner / a.x_cg, a.x_cg_stride, N, a.xsi,
+  if (a.wht_grp) {
+    // (maps built above)
+  } else if (a.x_cg ? !make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.inner / a.x_cg, a.x_cg_stride, N, a.xsi,
                               a.n2 * a.x_cg, G::CT, a.wht_half == 1 ? rlo : 0, a.wht_half == 1 ? ein : 0,
                               a.wht_half == 1)
              : !make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT,
@@ -583,11 +648,12 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
     return false;
   // TMA-store epilogue when the output view is TMA-compatible as well
   const bool ts = eout > 0 &&
-                  (a.y_cg ? make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.inner / a.y_cg, a.y_cg_stride, N,
+                  (a.wht_grp ? true
+                   : a.y_cg ? make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.inner / a.y_cg, a.y_cg_stride, N,
                                           a.ysi, a.n2 * a.y_cg, G::CT)
                           : make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
                                           blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc, blo ? a.ysi_hi : 0));
-  if (!ts && (blo || a.y_cg)) return false;  // direct stores are single-level, ungrouped
+  if (!ts && (blo || a.y_cg || a.wht_grp)) return false;  // direct stores are single-level, ungrouped
   if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;
@@ -629,6 +695,13 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   using F_ = std::false_type;
   using W0 = std::integral_constant<int, 0>;
   auto pick2 = [&](auto ts_tag) -> bool {
+    if (a.wht_grp) {
+      if constexpr (decltype(ts_tag)::value && (CTO == 32 || CTO == 64) && G::CT == CTO && N <= 256) {
+        using W3 = std::integral_constant<int, 3>;
+        return a.mid ? pick(ts_tag, T_{}, F_{}, F_{}, W3{}) : pick(ts_tag, F_{}, F_{}, F_{}, W3{});
+      }
+      return false;
+    }
     if (msk) {
       if (a.tw_on) {
         // (the fused Walsh-Hadamard variants: complex128 passes of the C5 chain)
@@ -665,6 +738,15 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
 // passes.
 template <class C, int N>
 inline bool fft_tma_launch(const FftArgs& a, cudaStream_t s) {
+  // (the fused Kron Walsh-Hadamard passes, complex64: 128 points on 64-column
+  // tiles — 8 columns x 8 hh, 64-byte rows — and 256 points on 32-column tiles)
+  if constexpr (sizeof(C) == 8 && N == 128) {
+    if (a.wht_grp) return fft_tma_launch_v<C, N, 16, 0, 64>(a, s);
+  }
+  if constexpr (sizeof(C) == 8 && N == 256) {
+    if (a.wht_grp) return fft_tma_launch_v<C, N, 16, 0, 32>(a, s);
+  }
+  if (a.wht_grp) return false;
   if constexpr (N == 1024 && sizeof(C) == 16) {
     if (!a.mid) return fft_tma_launch_v<C, N, 16, 1>(a, s);
   }
