@@ -624,7 +624,10 @@ def run_native(args, cfg):
     # end to end through the public API with pinned HOST buffers
     e2e = None
     if not args.no_e2e:
-        Xh = torch.from_numpy(Xh_local).pin_memory()
+        # this rank's column slice as a strided view of the whole pinned host
+        # block: the host path stages it with pitched copies (ABI ldx), no
+        # host-side repacking inside or outside the timed region
+        Xh = torch.from_numpy(np.ascontiguousarray(w.X)).pin_memory()[:, a:b]
         e_steps = 3
         for _ in range(2):  # the pinned caching allocator holds the blocks the loop cycles through
             yh = op.forward(Xh)
