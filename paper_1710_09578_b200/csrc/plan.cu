@@ -1407,6 +1407,10 @@ struct KronNode : Node {
     return h && h->order == 6 && fft_leaf(f[1]) && fft_leaf(f[2]);
   }
   void run_fused(Ctx& c, bool adj, const Blk& x, const Blk& y, const Geo& g) {
+    struct Clear {  // (the fused-WHT request never outlives this call)
+      Ctx& c;
+      ~Clear() { c.wgrp = 0; }
+    } clear{c};
     const int64_t ic = g.inner, na = f[1]->rows, nb = f[2]->rows, plane = na * nb * ic;
     Geo gt;
     gt.inner = ic;
@@ -1427,7 +1431,6 @@ struct KronNode : Node {
     c.wgrp = 3; c.wg_xs = c.wg_ys = 8 * plane; c.wg_used = false;
     f[1]->apply(c, adj, t2, y2, g2, false);
     SMAT_CHECK(c.wg_used, SMAT_UNSUPPORTED, "kron: fused Walsh-Hadamard not taken");
-    c.wgrp = 0;
   }
   // whether both fused passes run (a launcher probe, cached per direction and width)
   mutable std::mutex fuse_mu;
