@@ -400,7 +400,6 @@ def pass_bytes(cfg: int, label: str, K: int) -> int | None:
     units: every operand block read or written once, parameters once)."""
     from paper_1710_09578_b200 import configs
 
-    label = label.replace("_cg", "")  # (same bytes with the column-grouped intermediate)
     if cfg == 1:
         return 2 * 1024 * K * 8
     if cfg == 2:

@@ -431,26 +431,13 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
   SMAT_CHECK(!io.y_blk || io.mid, SMAT_UNSUPPORTED, "blocked output rows need the convolution passes");
   constexpr int BL = 6;
   const int64_t B = int64_t(1) << BL;
-  // Column-grouped intermediate (complex128 convolutions, N2 = 1024): W is
-  // stored as [n1 / B][column group of 4][k2][n1 % B][4 columns] — the outer
-  // passes' tile (one n1, 4 columns) is then a 64-byte run 4 KB apart per k2,
-  // and a middle-pass tile (one k2, 2 columns) 32-byte runs 64 bytes apart,
-  // i.e. whole 64-byte segments shared by the tile pair, instead of 32 bytes
-  // every 2 KB (tools/layout_probe.cu: 5.0-5.7 vs 2.8-3.9 TB/s).  TMA passes
-  // only: used when all three passes qualify.
-  constexpr int64_t CG = 4;
-  const int64_t GN = ic / CG, PL = N2 * B * CG;
-  auto pass1 = [&](bool w4) {
+  auto pass1 = [&]() {
     FftArgs a;
     xform_pass_common(a, c);
     a.x = io.x.p; a.x_real = !dt_complex(io.x.dt);
     a.xs1 = B * io.x.si; a.xs2 = io.x.si; a.xsi = N1 * io.x.si;  // (n1 / B, n1 % B, k2)
     a.y = W.p; a.y_real = 0;
     a.ys1 = N2 * B * ic; a.ys2 = ic; a.ysi = B * ic;
-    if (w4) {
-      a.ys1 = GN * PL; a.ys2 = CG; a.ysi = B * CG;
-      a.y_cg = int32_t(CG); a.y_cg_stride = PL;
-    }
     if (io.x_blk) {  // x in the blocked row layout too
       a.xs1 = io.blk_n2b * B * ic; a.xs2 = ic; a.xsi = B * ic;
     }
@@ -468,7 +455,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     return a;
   };
   const bool tw3 = tw_in_pass3(dbl, N1);
-  auto pass2 = [&](bool w4) {  // convolution: W -> W
+  auto pass2 = [&]() {  // convolution: W -> W
     FftArgs a;
     xform_pass_common(a, c);
     a.x = W.p; a.y = W.p;
@@ -480,11 +467,6 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
       a.xs2 = a.ys2 = B * ic;
       a.i_lo_bits = BL; a.xsi_hi = a.ysi_hi = N2 * B * ic;
     }
-    if (w4) {  // batch (column group, k2, column % 4); rows n1 % B, n1 / B
-      a.xs1 = a.ys1 = PL; a.xs2 = a.ys2 = B * CG; a.xsi = a.ysi = CG;
-      a.xsi_hi = a.ysi_hi = GN * PL;
-      a.inner = CG; a.g_div = CG;
-    }
     // spectra longer than one tile are stored in four-step order
     // (spec_fs[k2*N1 + k1] = spec[k2 + N2*k1], see spectrum_for_plan)
     a.mid = io.mid; a.mid_conj = io.mid_conj; a.mid_stride = 1; a.mid_gmul = N1;
@@ -494,7 +476,7 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     }
     return a;
   };
-  auto pass3 = [&](bool w4) {  // W -> y
+  auto pass3 = [&]() {  // W -> y
     FftArgs a;
     xform_pass_common(a, c);
     a.x = W.p; a.x_real = 0;
@@ -504,10 +486,6 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.n2 = O; a.inner = N1 * ic; a.nb = O * N1 * ic;
     if (blk) {  // (n1 / B, n1 % B, k2) as in pass 1
       a.xs1 = N2 * B * ic; a.xs2 = ic; a.xsi = B * ic;
-      if (w4) {
-        a.xs1 = GN * PL; a.xs2 = CG; a.xsi = B * CG;
-        a.x_cg = int32_t(CG); a.x_cg_stride = PL;
-      }
       a.ys1 = B * io.y.si; a.ys2 = io.y.si; a.ysi = N1 * io.y.si;
       if (io.y_blk) {
         a.ys1 = io.blk_n2b * B * ic; a.ys2 = ic; a.ysi = B * ic;
@@ -532,23 +510,9 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.scale = io.scale; a.accumulate = io.acc;
     return a;
   };
-  bool w4 = blk && dbl && io.mid && N2 == 1024 && ic % CG == 0;
-  if (w4) {
-    auto ok = [&](FftArgs a, int64_t N) {
-      a.probe_only = 1;
-      try {
-        launch_fft_tile(cdt, int(N), a, c.stream);
-      } catch (const Error& e) {
-        if (e.code != SMAT_UNSUPPORTED) throw;
-        return false;
-      }
-      return true;
-    };
-    w4 = ok(pass1(true), N2) && ok(pass2(true), N1) && ok(pass3(true), N2);
-  }
   // ---- pass 1: x -> W
   if (blk) {
-    c.fft(cdt, int(N2), pass1(w4));
+    c.fft(cdt, int(N2), pass1());
   } else {
     FftArgs a;
     xform_pass_common(a, c);
@@ -587,8 +551,8 @@ static void run_xform(Ctx& c, int64_t Nt, Geo g, XformIO io) {
     a.scale = io.scale; a.accumulate = io.acc;
     c.fft(cdt, int(N1), a);
   } else {
-    c.fft(cdt, int(N1), pass2(w4));
-    c.fft(cdt, int(N2), pass3(w4));
+    c.fft(cdt, int(N1), pass2());
+    c.fft(cdt, int(N2), pass3());
   }
   c.release(m0);
 }

@@ -100,7 +100,6 @@ struct Ctx {
       const bool pad = (a.g_mod - 1) + (N - 1) * a.gin_stride >= a.n_valid_in;
       const bool trunc = (a.g_mod - 1) + (N - 1) * a.gout_stride >= a.n_valid_out;
       if (a.pre || a.post || pad || trunc) lab += "_msk";
-      if (a.x_cg || a.y_cg) lab += "_cg";  // (column-grouped intermediate side)
     }
     note(lab);
     if (!measure) {

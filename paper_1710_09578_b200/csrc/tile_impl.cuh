@@ -93,7 +93,7 @@ __device__ __forceinline__ int64_t row_off(int i, int32_t si, int64_t si_hi, int
 enum : uint32_t {
   F_XREAL = 1, F_YREAL = 2, F_CONJX = 4, F_CONJY = 8, F_INV = 16, F_MIDCONJ = 32, F_TWINV = 64,
   F_ACC = 128, F_PRECONJ = 256, F_POSTCONJ = 512, F_PAD = 1024, F_TRUNC = 2048, F_SCALE = 4096,
-  F_GOFF = 8192, F_TWPRE = 16384, F_XCG = 1u << 22, F_YCG = 1u << 23
+  F_GOFF = 8192, F_TWPRE = 16384
 };
 
 struct WhtDev {

@@ -68,7 +68,6 @@ void launch_fft_tile(int cdt, int N, const FftArgs& a, cudaStream_t s) {
     if (cdt == SMAT_C128 && launch_fft_tma_c128(N, a, s)) return;
   }
   SMAT_CHECK(!a.wht_half, SMAT_UNSUPPORTED, "fused Walsh-Hadamard stages need the TMA pass");
-  SMAT_CHECK(!a.x_cg && !a.y_cg, SMAT_UNSUPPORTED, "column-grouped views need the TMA pass");
   SMAT_CHECK(!a.wht_grp, SMAT_UNSUPPORTED, "fused Kron Walsh-Hadamard needs the TMA pass");
   if (a.probe_only) return;
   if (cdt == SMAT_C64) {

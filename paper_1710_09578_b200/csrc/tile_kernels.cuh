@@ -65,12 +65,6 @@ struct FftArgs {
   // padded Hadamard): 1 = on the loaded input, before the masks / pre vector
   // and the FFT; 2 = on the output, after the post vector, before the store
   int32_t wht_half = 0;
-  // column-grouped side (the complex128 four-step intermediate of the
-  // convolution passes, run_xform): when x_cg (y_cg) > 0, column c of a batch
-  // sits at (c / cg) * cg_stride + c % cg, and the o2 index (stride xs2 == cg)
-  // with c % cg forms one contiguous run — TMA kernel only, cg == its column tile
-  int32_t x_cg = 0, y_cg = 0;
-  int64_t x_cg_stride = 0, y_cg_stride = 0;
   // fused 8-point Walsh-Hadamard across a batch index (Kron(Hadamard, ...),
   // KronNode): the batch's inner index is virtual, v = (column group of 4,
   // hh, column % 4) with hh (element strides wg_xs / wg_ys) the Hadamard

@@ -134,7 +134,7 @@ __device__ __forceinline__ void wht_lanes8(C* a) {
 
 // launcher-only flags of the TMA pass: the pre (post) vector is stored per
 // tile (pre_gmul / post_gmul) and rides with the tile as a bulk-loaded slice
-enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21, F_TSWZ = 1u << 24, F_WGRP = 1u << 25 };
+enum : uint32_t { F_SIDEPRE = 1u << 20, F_SIDEPOST = 1u << 21, F_WGRP = 1u << 25 };
 
 // MSK: the masked variant for the Bluestein / pruned-embedding passes — zero
 // padding of input rows (g = goff + i*gin_stride >= n_valid_in), truncation of
@@ -180,29 +180,17 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   const R smid = (f & F_MIDCONJ) ? R(-1) : R(1);
 
   const bool side_pre = MSK && (f & F_SIDEPRE) != 0, side_post = MSK && (f & F_SIDEPOST) != 0;
-  // first batch of tile t: t*CT, or (column-grouped passes, F_TSWZ) the
-  // o2 index fastest, then the column group, then o1 — the tiles in flight
-  // then share the column-grouped side's 4 KB rows
-  auto tile_b0 = [&](int t) -> uint32_t {
-    if (!(f & F_TSWZ)) return uint32_t(t) * CT;
-    const uint32_t q = fdiv(uint32_t(t), p.n2.m, p.n2.s), lo = uint32_t(t) - q * p.n2.d;
-    const uint32_t ng = p.inner.d / CT, o1 = q / ng, g = q - o1 * ng;
-    return (o1 * p.n2.d + lo) * p.inner.d + g * CT;
-  };
   auto tile_goff = [&](int t) -> int {
-    const uint32_t q = fdiv(tile_b0(t), p.gdiv.m, p.gdiv.s);
+    const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
     return int(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
   };
   auto issue = [&](int t, int s) {
     uint32_t o1, o2, c0;
-    decode_batch(tile_b0(t), p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
+    decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
     const uint32_t sb = MID ? uint32_t(N * sizeof(C)) : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
     // (a masked box moves only the ein rows every tile owns)
     mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
-    // (a column-grouped side: the tile's (o2, column group) run, see FftArgs::x_cg)
-    if (f & F_XCG)
-      tma_load_5d(stage_buf(s), &xmap, &bars[s], int(o2 * CT * (sizeof(C) / 8)), 0, 0, int(c0 / CT), int(o1));
-    else if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
+    if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
       tma_load_5d(stage_buf(s), &xmap, &bars[s], int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
     else
       tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
@@ -228,7 +216,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   const int prow = ein + tid / CT, pcol = tid % CT;
   auto patch_load = [&](int t) -> C {
     uint32_t o1, o2, c0;
-    decode_batch(tile_b0(t), p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
+    decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
     int v = N;
     if (f & F_PAD) {
       const int rem = p.n_valid_in - tile_goff(t);
@@ -258,7 +246,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   C tvlo[TW && !TVSL ? PER : 1], tvhi[TW && !TVSL ? PER : 1];
   auto tv_prefetch = [&](int t) {
     if constexpr (TW && !TVSL) {
-      const uint32_t q = fdiv(tile_b0(t), p.gdiv.m, p.gdiv.s);
+      const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
       const uint32_t g32 = q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d;
       const C* thi = (const C*)p.tw_hi;
       const C* tlo = (const C*)p.tw_lo;
@@ -305,7 +293,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
 
   for (int t = blockIdx.x, it = 0; t < ntiles; t += gs, ++it) {
     // ---- per-thread batch geometry
-    const uint32_t b = tile_b0(t) + cs;
+    const uint32_t b = uint32_t(t) * CT + cs;
     uint32_t o1, o2, c;
     decode_batch(b, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c);
     const int64_t yb = int64_t(o1) * p.ys1 + int64_t(o2) * p.ys2 + c;
@@ -532,10 +520,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       __syncthreads();
       if (tid == 0) {
         uint32_t q1, q2, c0;
-        decode_batch(tile_b0(t), p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, q1, q2, c0);
-        if (f & F_YCG)
-          tma_store_5d(&ymap, buf, int(q2 * CT * (sizeof(C) / 8)), 0, 0, int(c0 / CT), int(q1));
-        else if (f & F_WGRP)
+        decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, q1, q2, c0);
+        if (f & F_WGRP)
           tma_store_5d(&ymap, buf, int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
         else
           tma_store_5d(&ymap, buf, int(c0 * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
@@ -596,9 +582,6 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   }
   FftDev d = d0;
   if (a.wht_grp) d.flags |= F_WGRP;
-  if (a.x_cg) d.flags |= F_XCG;
-  if (a.y_cg) d.flags |= F_YCG;
-  if (a.x_cg || a.y_cg) d.flags |= F_TSWZ;
   if (msk && a.pre && a.pre_gmul) d.flags |= F_SIDEPRE;
   else if (msk && a.post && a.post_gmul) d.flags |= F_SIDEPOST;
   const int64_t n1 = a.nb / (a.n2 * a.inner);
@@ -610,7 +593,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   if (a.wht_grp) {
     // fused Kron Walsh-Hadamard: both sides as {columns, hh, rows, o2, o1}
     // with 4-column x 8-hh boxes (single-dimension rows: N <= 256)
-    if ((G::CT != 32 && G::CT != 64) || N > 256 || msk || a.tw_on || blo || a.x_cg || a.y_cg || a.wht_half ||
+    if ((G::CT != 32 && G::CT != 64) || N > 256 || msk || a.tw_on || blo || a.wht_half ||
         a.inner % G::CT || a.x_real || a.y_real)
       return false;
     const int64_t ic = a.inner / 8;
@@ -634,26 +617,19 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
       return false;
   }
   const bool pin = pad || a.wht_half == 1;
-  // column-grouped sides: one column tile per group, the o2 rows and the
-  // group's columns contiguous, no masked rows (every access is a TMA box)
-  if (a.x_cg && (a.x_cg != G::CT || a.xs2 != a.x_cg || blo || pad || a.inner % a.x_cg)) return false;
-  if (a.y_cg && (a.y_cg != G::CT || a.ys2 != a.y_cg || blo || trunc || a.inner % a.y_cg)) return false;
   if (a.wht_grp) {
     // (maps built above)
-  } else if (a.x_cg ? !make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.inner / a.x_cg, a.x_cg_stride, N, a.xsi,
-                              a.n2 * a.x_cg, G::CT, a.wht_half == 1 ? rlo : 0, a.wht_half == 1 ? ein : 0,
-                              a.wht_half == 1)
-             : !make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT,
-                              blo ? blo : pin ? rlo : 0, pin ? ein : 0, pin, blo ? a.xsi_hi : 0))
+  } else if (!make_view_map(&map, a.x, sizeof(C), n1, a.xs1, a.n2, a.xs2, N, a.xsi, a.inner, G::CT,
+                            blo ? blo : pin ? rlo : 0, pin ? ein : 0, pin, blo ? a.xsi_hi : 0)) {
     return false;
+  }
   // TMA-store epilogue when the output view is TMA-compatible as well
   const bool ts = eout > 0 &&
                   (a.wht_grp ? true
-                   : a.y_cg ? make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.inner / a.y_cg, a.y_cg_stride, N,
-                                          a.ysi, a.n2 * a.y_cg, G::CT)
-                          : make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
-                                          blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc, blo ? a.ysi_hi : 0));
-  if (!ts && (blo || a.y_cg || a.wht_grp)) return false;  // direct stores are single-level, ungrouped
+                             : make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
+                                             blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc,
+                                             blo ? a.ysi_hi : 0));
+  if (!ts && (blo || a.wht_grp)) return false;  // direct stores are single-level, ungrouped
   if (!ts) ymap = map;
   const int64_t ntiles = a.nb / G::CT;
   if (ntiles <= 0) return true;
