@@ -88,7 +88,8 @@ struct WlrGeom {
   static constexpr int DATA = TR * DP;
   static constexpr int FACT = TR * FP;
   static constexpr int NBAR = NSD + NSF + NGRP;
-  static constexpr int SMEM = NSD * DATA + NSF * FACT + NBAR * 8;
+  static constexpr int ROWT = NGRP * TR * 8;  // per group: the unit's output row offsets
+  static constexpr int SMEM = NSD * DATA + NSF * FACT + ROWT + NBAR * 8;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -176,7 +177,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* dring = smem;                  // data tiles
   unsigned char* fring = smem + NSD * G::DATA;  // factor rows
-  uint64_t* full = reinterpret_cast<uint64_t*>(fring + NSF * G::FACT);
+  int64_t* rowt = reinterpret_cast<int64_t*>(fring + NSF * G::FACT);  // [NGRP][TR]
+  uint64_t* full = reinterpret_cast<uint64_t*>(fring + NSF * G::FACT + G::ROWT);
   uint64_t* ffull = full + NSD;
   uint64_t* mma_done = ffull + NSF;  // per group: its tensor phase of a unit is issued
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -297,6 +299,9 @@ __global__ void __launch_bounds__(NTHR, 1)
       group_sync(grp);
     }
     const int rf = rows_valid(min(a.n_f, a.nrows), g0);
+    // the unit's output row offsets, once per unit (read by the stores after
+    // the group barriers of the tensor phase / transform)
+    if (OUT && gt < TR) rowt[grp * TR + gt] = wlr_phys<NW>(a.yout, g0 + gt) * a.yout.ld + c0;
 
     if constexpr (CON) mma_acquire(i, fbuf, rf);
     if constexpr (CON && !(WLR_SKIP & 1)) {
@@ -349,13 +354,15 @@ __global__ void __launch_bounds__(NTHR, 1)
     if constexpr (EXP && !(WLR_SKIP & 4)) {
       // Y[t][c] += sum_q G[t][q] W'[q][c]  (warp: 8 columns; rows in quarters)
       //   T1 = Gr Wr, T2 = Gi Wi, T3 = (Gr + Gi)(Wr + Wi):  Re = T1 - T2, Im = T3 - T1 - T2
-#pragma unroll 1
-      for (int qr = 0; qr < 4; ++qr) {
-        double e[2][3][2];
+      // Quarter qr + 1's products are issued before quarter qr's rows are
+      // read-modified-written, so the shared-memory update runs under the
+      // tensor work; the tensor phase is released before the last update.
+      double e[2][2][3][2];
+      auto mma_q = [&](int qr, double (&eq)[2][3][2]) {
 #pragma unroll
         for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-          for (int p = 0; p < 3; ++p) e[i2][p][0] = e[i2][p][1] = 0.0;
+          for (int p = 0; p < 3; ++p) eq[i2][p][0] = eq[i2][p][1] = 0.0;
         // (k-step ks + 1's factor entries and sums are formed while ks multiplies)
         const unsigned char* g0p = fbuf + (16 * qr + (lane >> 2)) * FP + (lane & 3) * 16;
         double2 gv[2];
@@ -376,11 +383,13 @@ __global__ void __launch_bounds__(NTHR, 1)
           }
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
-            dmma(e[mt][0], gc[mt].x, wb[ks][0]);
-            dmma(e[mt][1], gc[mt].y, wb[ks][1]);
-            dmma(e[mt][2], gs2[mt], wb[ks][2]);
+            dmma(eq[mt][0], gc[mt].x, wb[ks][0]);
+            dmma(eq[mt][1], gc[mt].y, wb[ks][1]);
+            dmma(eq[mt][2], gs2[mt], wb[ks][2]);
           }
         }
+      };
+      auto rmw_q = [&](int qr, const double (&eq)[2][3][2]) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           const int row = 16 * qr + 8 * mt + (lane >> 2);
@@ -388,19 +397,27 @@ __global__ void __launch_bounds__(NTHR, 1)
           for (int j = 0; j < 2; ++j) {
             unsigned char* pp = dbuf + row * DP + (8 * gw + 2 * (lane & 3) + j) * 16;
             const double2 v = ld2(pp);
-            st2(pp, make_double2(v.x + e[mt][0][j] - e[mt][1][j], v.y + e[mt][2][j] - e[mt][0][j] - e[mt][1][j]));
+            st2(pp, make_double2(v.x + eq[mt][0][j] - eq[mt][1][j], v.y + eq[mt][2][j] - eq[mt][0][j] - eq[mt][1][j]));
           }
         }
+      };
+      mma_q(0, e[0]);
+#pragma unroll
+      for (int qr = 0; qr < 4; ++qr) {
+        if (qr + 1 < 4) mma_q(qr + 1, e[(qr + 1) & 1]);
+        else mma_release(i);
+        rmw_q(qr, e[qr & 1]);
       }
+      group_sync(grp);  // (the expanded rows are complete before the stores read them)
+    } else if constexpr (EXP) {
+      mma_release(i);
     }
-    if constexpr (EXP) mma_release(i);  // (also: the expanded rows are written)
     if constexpr (OUT && !(WLR_SKIP & 8)) {
       // thread: column c, rows t = gt / 32 + 4 j (coalesced 512-byte rows)
       const int rout = rows_valid(min(a.n_out, a.nrows), g0);
       const int c = gt % KC;
       if (c < kcv) {
-        for (int t = gt / KC; t < rout; t += GTHR / KC)
-          Y[wlr_phys<NW>(a.yout, g0 + t) * a.yout.ld + c0 + c] = ld2(dbuf + t * DP + c * 16);
+        for (int t = gt / KC; t < rout; t += GTHR / KC) Y[rowt[grp * TR + t] + c] = ld2(dbuf + t * DP + c * 16);
       }
     }
     // stage s is free: order this group's generic-proxy accesses before the
