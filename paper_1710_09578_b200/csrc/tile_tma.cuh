@@ -88,12 +88,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // strides 1, 8, 64, ... (stride-1-first); TPC threads per column hold 8
 // elements each (N/2 = 8 TPC).  The load order of each group is rotated by the
 // group index so that the two row groups a memory phase touches differ.
-template <class C, int N, int CT, int TPC, int S = 1>
+// SMAX: the strides handled here (the stages with stride >= SMAX = TPC — the
+// bits of the stage-0 element index r — run in registers on the loaded /
+// finished elements instead, wht_regs_half).
+template <class C, int N, int CT, int TPC, int S = 1, int SMAX = N / 2>
 __device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
   constexpr int NH = N / 2;
   static_assert(NH == 8 * TPC, "8 elements per thread");
-  if constexpr (S < NH) {
-    constexpr int R = NH / S >= 8 ? 8 : NH / S;
+  if constexpr (S < SMAX) {
+    constexpr int R = SMAX / S >= 8 ? 8 : SMAX / S;
 #pragma unroll
     for (int q = 0; q < 8 / R; ++q) {
       const int gid = j + q * TPC;
@@ -106,8 +109,17 @@ __device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
       for (int k = 0; k < R; ++k) buf[(base + k * S) * CT + cs] = v[k];
     }
     __syncthreads();
-    tile_wht_half<C, N, CT, TPC, S * R>(buf, j, cs);
+    tile_wht_half<C, N, CT, TPC, S * R, SMAX>(buf, j, cs);
   }
+}
+
+// The remaining Walsh-Hadamard stage of tile_wht_half<..., SMAX = TPC>: a
+// thread's stage-0 elements a[r] are rows j + TPC r, so rows < N/2 are r < 8
+// and their stride-TPC.. bits are the bits of r — an 8-point transform in
+// registers (one shared-memory round trip and barrier fewer).
+template <class C>
+__device__ __forceinline__ void wht_regs_half(C* a) {
+  wht_small<8>(a);
 }
 
 // 8-point Walsh-Hadamard over the Kron Hadamard index hh of a tile whose
@@ -347,7 +359,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         if (powner && t + gs < ntiles) pval = patch_load(t + gs);
       }
     }
-    if constexpr (WH == 1 && !(FFT_SKIP & 2)) tile_wht_half<C, N, CT, TPC>(buf, j, cs);  // (ends with a barrier)
+    // (the fused half Walsh-Hadamard: strides < TPC in shared memory, the
+    // rest in registers once loaded; the row mask applies after it)
+    constexpr bool WHREG = (WH == 1 || WH == 2) && R0 == E && N / R0 == TPC && RL == E;
+    if constexpr (WH == 1 && !(FFT_SKIP & 2)) {
+      if constexpr (WHREG) tile_wht_half<C, N, CT, TPC, 1, TPC>(buf, j, cs);  // (ends with a barrier)
+      else tile_wht_half<C, N, CT, TPC>(buf, j, cs);
+    }
     C a[E];
 #pragma unroll
     for (int u = 0; u < E / R0; ++u)
@@ -359,10 +377,18 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
           // (hh's top bit, cs bit 5: own and partner column of the landed row)
           const C o = buf[i * CT + cs], q = buf[i * CT + (cs ^ 32)];
           a[u * R0 + r] = (cs & 32) ? q - o : o + q;
+        } else if constexpr (WH == 1 && WHREG) {
+          a[u * R0 + r] = buf[i * CT + cs];
         } else {
           a[u * R0 + r] = (!MSK || i < vin) ? buf[i * CT + cs] : C{};
         }
       }
+    if constexpr (WH == 1 && WHREG) {
+      if constexpr (!(FFT_SKIP & 2)) wht_regs_half(a);
+#pragma unroll
+      for (int r = 0; r < E; ++r)
+        if (MSK && !(j + r * TPC < vin)) a[r] = C{};
+    }
     if ((MSK && p.pre) || twpre) {
       // conj_x, the pre vector, the input twiddle, then the inverse conjugation
       if (f & F_CONJX) {
@@ -492,6 +518,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
           au[r].y *= s_im;
         }
       }
+      if constexpr (WH == 2 && WHREG && !(FFT_SKIP & 2)) wht_regs_half(au);
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
         const int k = bb + r * (N / RL);
@@ -514,7 +541,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     if constexpr (TS) {
       if constexpr (WH == 2 && !(FFT_SKIP & 2)) {
         __syncthreads();
-        tile_wht_half<C, N, CT, TPC>(buf, j, cs);
+        if constexpr (WHREG) tile_wht_half<C, N, CT, TPC, 1, TPC>(buf, j, cs);
+        else tile_wht_half<C, N, CT, TPC>(buf, j, cs);
       }
       fence_proxy_async();  // this thread's tile writes -> visible to the TMA engine
       __syncthreads();
