@@ -317,13 +317,17 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     // valid input rows i < vin, output rows k < vout of this tile
     int vin = N, vout = N;
     if constexpr (MSK) {
+      // (ceil(rem / stride); the four-step strides are powers of two: a shift)
+      auto cdiv = [](int rem, int st) {
+        return (st & (st - 1)) == 0 ? (rem + st - 1) >> (__ffs(st) - 1) : (rem + st - 1) / st;
+      };
       if (f & F_PAD) {
         const int rem = p.n_valid_in - goff;
-        vin = rem <= 0 ? 0 : min(N, (rem + p.gin_stride - 1) / p.gin_stride);
+        vin = rem <= 0 ? 0 : min(N, cdiv(rem, p.gin_stride));
       }
       if (f & F_TRUNC) {
         const int rem = p.n_valid_out - goff;
-        vout = rem <= 0 ? 0 : min(N, (rem + p.gout_stride - 1) / p.gout_stride);
+        vout = rem <= 0 ? 0 : min(N, cdiv(rem, p.gout_stride));
       }
     }
     if constexpr (TW && !TVSL) {
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         } else if constexpr (WH == 1 && WHREG) {
           a[u * R0 + r] = buf[i * CT + cs];
         } else {
+          // (rows past the tile's valid count were not loaded: zero padding)
           a[u * R0 + r] = (!MSK || i < vin) ? buf[i * CT + cs] : C{};
         }
       }
@@ -405,7 +410,9 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
 #pragma unroll
             for (int r = 0; r < R0; ++r) {
               const int i = j + u * TPC + r * (N / R0);
-              if (i < vin) {
+              // (a per-tile slice is zero past the vector's end, and so are
+              // the input rows: no guard needed there)
+              if (side_pre || i < vin) {
                 const C w = side_pre ? ps[i] : __ldg(&pv[p.pre_gmul ? goff * p.pre_gmul + i : goff + i * p.gin_stride]);
                 a[u * R0 + r] = pc ? cmulc(a[u * R0 + r], w) : cmul(a[u * R0 + r], w);
               }
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
 #pragma unroll
           for (int r = 0; r < RL; ++r) {
             const int k = bb + r * (N / RL);
-            if (k < vout) {
+            if (side_post || k < vout) {  // (rows >= vout are never stored)
               const C w = side_post ? qs[k]
                                     : __ldg(&qv[p.post_gmul ? goff * p.post_gmul + k : goff + k * p.gout_stride]);
               au[r] = qc ? cmulc(au[r], w) : cmul(au[r], w);
@@ -524,10 +531,19 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         const int k = bb + r * (N / RL);
         if constexpr (TS) {
           buf[k * CT + cs] = au[r];
-          // rows eout <= k < vout lie outside the store map: write them directly
-          if (MSK && k >= eout && k < vout) yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
         } else if (!MSK || k < vout) {
           yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+        }
+      }
+      if constexpr (MSK && TS) {
+        // rows eout <= k < vout lie outside the store map: the tiles that own
+        // such rows write them directly
+        if (vout > eout) {
+#pragma unroll
+          for (int r = 0; r < RL; ++r) {
+            const int k = bb + r * (N / RL);
+            if (k >= eout && k < vout) yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+          }
         }
       }
     }
