@@ -390,9 +390,15 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       }
     if constexpr (WH == 1 && WHREG) {
       if constexpr (!(FFT_SKIP & 2)) wht_regs_half(a);
+      // rows >= N/2 (r >= 8) were not loaded; rows vin.. of the first half
+      // are truncated Hadamard outputs
 #pragma unroll
-      for (int r = 0; r < E; ++r)
-        if (MSK && !(j + r * TPC < vin)) a[r] = C{};
+      for (int r = 8; r < E; ++r) a[r] = C{};
+      if (vin < N / 2) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (!(j + r * TPC < vin)) a[r] = C{};
+      }
     }
     if ((MSK && p.pre) || twpre) {
       // conj_x, the pre vector, the input twiddle, then the inverse conjugation
@@ -474,16 +480,27 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
             a[u * RF + r] = mc ? cmul_f2(conj(v), w) : conj(cmul_f2(v, w));
           }
       } else {
+        // conj(a s) or conj(a conj(s)), the sign chosen once per tile
         const C* mid = reinterpret_cast<const C*>(stage_spec(sidx));
+        if (smid < R(0)) {
 #pragma unroll
-        for (int u = 0; u < E / RF; ++u)
+          for (int u = 0; u < E / RF; ++u)
 #pragma unroll
-          for (int r = 0; r < RF; ++r) {
-            const int k = j + u * TPC + r * (N / RF);
-            C sv = mid[k];
-            sv.y *= smid;
-            a[u * RF + r] = conj(cmul(a[u * RF + r], sv));
-          }
+            for (int r = 0; r < RF; ++r) {
+              const C sv = mid[j + u * TPC + r * (N / RF)];
+              C& v = a[u * RF + r];
+              v = mk(fma(v.x, sv.x, v.y * sv.y), fma(v.x, sv.y, -v.y * sv.x));
+            }
+        } else {
+#pragma unroll
+          for (int u = 0; u < E / RF; ++u)
+#pragma unroll
+            for (int r = 0; r < RF; ++r) {
+              const C sv = mid[j + u * TPC + r * (N / RF)];
+              C& v = a[u * RF + r];
+              v = mk(fma(v.x, sv.x, -v.y * sv.y), fma(-v.x, sv.y, -v.y * sv.x));
+            }
+        }
       }
       if constexpr (!(FFT_SKIP & 1)) fft_stages<C, N, E, CT, true, 0, LAY, N, true, MID>(a, buf, j, cs, tws_mir);
     }
