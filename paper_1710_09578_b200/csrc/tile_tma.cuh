@@ -469,16 +469,20 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       if constexpr (sizeof(C) == 8) {
         // plain spectrum: conj(a*s) = conj(a s); conj(a*conj s) = conj(a) s
         const float2* ms = reinterpret_cast<const float2*>(stage_spec(sidx));
-        const bool mc = (f & F_MIDCONJ) != 0;
+        // (the conjugation variant chosen once per tile, not per element)
+        if ((f & F_MIDCONJ) != 0) {
 #pragma unroll
-        for (int u = 0; u < E / RF; ++u)
+          for (int u = 0; u < E / RF; ++u)
 #pragma unroll
-          for (int r = 0; r < RF; ++r) {
-            const int k = j + u * TPC + r * (N / RF);
-            const float2 w = ms[k];
-            C v = a[u * RF + r];
-            a[u * RF + r] = mc ? cmul_f2(conj(v), w) : conj(cmul_f2(v, w));
-          }
+            for (int r = 0; r < RF; ++r)
+              a[u * RF + r] = cmul_f2(conj(a[u * RF + r]), ms[j + u * TPC + r * (N / RF)]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < E / RF; ++u)
+#pragma unroll
+            for (int r = 0; r < RF; ++r)
+              a[u * RF + r] = conj(cmul_f2(a[u * RF + r], ms[j + u * TPC + r * (N / RF)]));
+        }
       } else {
         // conj(a s) or conj(a conj(s)), the sign chosen once per tile
         const C* mid = reinterpret_cast<const C*>(stage_spec(sidx));
