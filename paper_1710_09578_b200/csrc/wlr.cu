@@ -191,6 +191,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   // this CTA's units: blockIdx.x + i * gs, i < nloc (gs is a multiple of
   // nchunks, so every unit of the CTA is in column chunk ch)
   const int nloc = int(blockIdx.x) < nunits ? (nunits - 1 - int(blockIdx.x)) / gs + 1 : 0;
+  // first unit row of the CTA's i-th unit: unit u = blockIdx.x + i gs covers
+  // row block u / nchunks = blockIdx.x / nchunks + i (gs / nchunks)
+  const int rb0 = int(blockIdx.x) / nchunks, rbs = gs / nchunks;
+  auto unit_g0 = [&](int i) -> int64_t { return int64_t(rb0 + i * rbs) * TR; };
   double2* Y = reinterpret_cast<double2*>(a.y);
   const double2* F = reinterpret_cast<const double2*>(a.F);
   const int lgw = a.in.kind == WLR_IN_ROWS ? 0 : ilog2_dev(int(a.in.nwa));
@@ -211,8 +215,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   // factor rows (one bulk copy of the padded rows) into factor stage i % NSF
   auto issue_data = [&](int i) {
     if constexpr (IN) {
-      const int u = int(blockIdx.x) + i * gs;
-      const int64_t g0 = int64_t(u / nchunks) * TR;
+      const int64_t g0 = unit_g0(i);
       const int s = i % NSD;
       unsigned char* dbuf = dring + s * G::DATA;
       mbar_arrive_expect_tx(&full[s], uint32_t(G::DATA));
@@ -229,8 +232,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
   };
   auto issue_factor = [&](int i) {
-    const int u = int(blockIdx.x) + i * gs;
-    const int64_t g0 = int64_t(u / nchunks) * TR;
+    const int64_t g0 = unit_g0(i);
     const int sf = i % NSF;
     const int rf = rows_valid(min(a.n_f, a.nrows), g0);
     const uint32_t fbytes = uint32_t(rf) * FP;
@@ -287,10 +289,9 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   for (int i = grp; i < nloc; i += NGRP) {
     const int s = i % NSD, sf = i % NSF;
-    const int u = int(blockIdx.x) + i * gs;
     unsigned char* dbuf = dring + s * G::DATA;
     unsigned char* fbuf = fring + sf * G::FACT;
-    const int64_t g0 = int64_t(u / nchunks) * TR;
+    const int64_t g0 = unit_g0(i);
     if constexpr (IN) {
       mbar_wait(&full[s], uint32_t((i / NSD) & 1));
     } else {
