@@ -561,3 +561,40 @@ def test_column_major_and_staged_views():
     _close(sm.Hadamard(14).forward(A[:, 2:7]), orc.apply(oo, A[:, 2:7], 0), 0, "numpy slice")
     F = np.asfortranarray(A)
     _close(sm.Hadamard(14).forward(F), orc.apply(oo, A, 0), 0, "numpy fortran")
+
+
+def test_toeplitz_single_precision_shapes():
+    """Single precision Toeplitz with L = 8192 (the four-step convolution):
+    square and rectangular shapes, the 4096-row edge, complex64 data, an odd
+    real column count (no column-pair packing), accumulation inside a Sum, and
+    a strided column slice (leading dimension, transformed in place) against
+    the oracle."""
+    import torch
+
+    rng = np.random.default_rng(31)
+    for n, m, K, cplx in ((3000, 3000, 64, False), (4096, 4096, 6, False), (4000, 1500, 10, False),
+                          (1500, 4000, 4, False), (4096, 2, 2, False), (3000, 3000, 5, True),
+                          (2500, 3100, 3, True), (3000, 3000, 7, False)):
+        col = rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0)
+        row = rng.standard_normal(m - 1) + (1j * rng.standard_normal(m - 1) if cplx else 0)
+        dt = np.complex64 if cplx else np.float32
+        op = sm.Toeplitz(col.astype(dt), row.astype(dt))
+        ref = orc.toeplitz(col, row)
+        x = rng.standard_normal((m, K)) + (1j * rng.standard_normal((m, K)) if cplx else 0)
+        y = rng.standard_normal((n, K)) + (1j * rng.standard_normal((n, K)) if cplx else 0)
+        _close(op.forward(x.astype(dt)), orc.apply(ref, x), 1e-5, f"T{n}x{m} K{K} fwd")
+        _close(op.backward(y.astype(dt)), orc.apply(ref, y, 1), 1e-5, f"T{n}x{m} K{K} bwd")
+    # accumulation: Toeplitz + Diagonal
+    n = 3000
+    col, row = rng.standard_normal(n), rng.standard_normal(n - 1)
+    d = rng.standard_normal(n)
+    op = sm.Toeplitz(col.astype(np.float32), row.astype(np.float32)) + sm.Diagonal(d.astype(np.float32))
+    x = rng.standard_normal((n, 8))
+    want = orc.apply(orc.toeplitz(col, row), x) + d[:, None] * x
+    _close(op.forward(x.astype(np.float32)), want, 1e-5, "Toeplitz + Diagonal")
+    # strided column slice of a wider device block: transformed in place
+    t = sm.Toeplitz(col.astype(np.float32), row.astype(np.float32))
+    big = rng.standard_normal((n, 40)).astype(np.float32)
+    Xd = torch.from_numpy(big).cuda()[:, 4:36]
+    got = t.forward(Xd).cpu().numpy()
+    _close(got, orc.apply(orc.toeplitz(col, row), big[:, 4:36].astype(np.float64)), 1e-5, "strided slice")
