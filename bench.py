@@ -390,9 +390,15 @@ def _traffic(workload: str, kernel: str):
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+        per = json.loads(p.read_text()).get(workload, {})
     except (ValueError, AttributeError):
         return None
+    if kernel in per:
+        return per[kernel]
+    # (the launch lists name a kernel family by precision and length; the
+    # bench label adds the pass variant: fft_c128_2048 -> fft_c128_2048_spec)
+    fam = [k for k in per if kernel.startswith(k + "_")]
+    return per[max(fam, key=len)] if fam else None
 
 
 def pass_bytes(cfg: int, label: str, K: int) -> int | None:

@@ -21,6 +21,9 @@ def label(kernel: str):
     m = re.search(r"wht_tile_kernel<[^,]+, (\d+)", kernel)
     if m:
         return "wht_" + m.group(1)
+    m = re.search(r"wlr_kernel<(\d+),", kernel)
+    if m:  # (the C5 chain: N1 = 2048 = 32 (pass a) x 64 (pass b) unit-row groups)
+        return {"32": "wht_lowrank_a", "64": "wht_lowrank_b"}.get(m.group(1), "wlr_" + m.group(1))
     if "lr_contract_kernel" in kernel:
         return "lowrank_contract"
     if "lr_expand_kernel" in kernel:
