@@ -75,8 +75,14 @@ constexpr int FPE = (RK + 4) * 16;  // 576, expansion
 constexpr int GTHR = 128;                // threads per consumer group
 constexpr int NGRP = 2;                  // consumer groups
 constexpr int NTHR = NGRP * GTHR;
-constexpr int NSD = 4;                   // data ring stages
-constexpr int NSF = 2;                   // factor ring stages
+#ifndef WLR_NSD
+#define WLR_NSD 4
+#endif
+constexpr int NSD = WLR_NSD;             // data ring stages
+#ifndef WLR_NSF
+#define WLR_NSF 2
+#endif
+constexpr int NSF = WLR_NSF;             // factor ring stages
 // (timing experiments only, tools/exp_build.py: skip phases; results wrong)
 #ifndef WLR_SKIP
 #define WLR_SKIP 0
