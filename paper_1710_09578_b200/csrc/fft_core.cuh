@@ -240,9 +240,16 @@ __host__ __device__ constexpr int st_twoff(int N, int E, int s, bool mirror) {
 // Thread (j, cs) of a tile holds, at stage s (radix R, stride NS), the inputs
 // of butterflies bb = j + u*TPC (u < E/R): elements bb + r*N/R.  Outputs go to
 // (bb/NS)*NS*R + bb%NS + r*NS.  `tw` is W_TWN^t (t < TWN).
+// `hook` runs once the inputs of the LAST stage are in registers (after the
+// last exchange read; multi-stage transforms only): from there on the
+// exchange buffer is dead for this thread — the TMA pass refills it there.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
 template <class C, int N, int E, int CT, bool MIR, int S, int LAY = 0, int TWN = 4096, bool TWS = false,
-          bool TF2 = false>
-__device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* __restrict__ tw) {
+          bool TF2 = false, class Hook = NoHook>
+__device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* __restrict__ tw,
+                                           const Hook& hook = Hook{}) {
   constexpr int NST = st_count(N, E);
   if constexpr (S < NST) {
     constexpr int R = st_radix(N, E, S, MIR);
@@ -285,7 +292,8 @@ __device__ __forceinline__ void fft_stages(C* a, C* sm, int j, int cs, const C* 
 #pragma unroll
         for (int r = 0; r < R2; ++r) a[u * R2 + r] = sm[ex_row<LAY, SH>(bb + r * (N / R2)) * CT + cs];
       }
-      fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS, TF2>(a, sm, j, cs, tw);
+      if constexpr (S + 2 == NST) hook();
+      fft_stages<C, N, E, CT, MIR, S + 1, LAY, TWN, TWS, TF2, Hook>(a, sm, j, cs, tw, hook);
     }
   }
 }

@@ -79,6 +79,10 @@ struct TmaGeom {
 #define FFT_SKIP 0
 #endif
 
+#ifndef EARLY_SIDE
+#define EARLY_SIDE 1
+#endif
+
 template <class C, int N>
 constexpr bool kPdl = sizeof(C) == 8 && N <= 128;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   constexpr int R0 = st_radix(N, E, 0, false);
   constexpr int RL = MID ? st_radix(N, E, NST - 1, true) : st_radix(N, E, NST - 1, false);
   constexpr int LQ = log2_c(RL);
+  constexpr bool EARLY = !TS && !MID && MSK && TW && sizeof(C) == 16 && G::NBUF == 1 && NST >= 2 && G::TVSL && !(FFT_SKIP & 1);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // stage s: [tile data | spectrum slice] at smem_raw + s*STAGE
   auto stage_buf = [&](int s) { return reinterpret_cast<C*>(smem_raw + s * G::STAGE); };
@@ -196,30 +201,38 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
     return int(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
   };
-  auto issue = [&](int t, int s) {
+  // parts: 1 = the barrier's byte count and the tile box, 2 = the spectrum /
+  // pre / post slice, 4 = the four-step twiddle slice (the early-refill passes
+  // issue them apart: the box and the slice the prologue reads as soon as the
+  // landing buffer is dead, the slice the epilogue reads after it)
+  auto issue = [&](int t, int s, int parts = 7) {
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
     const uint32_t sb = MID ? uint32_t(N * sizeof(C)) : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
-    // (a masked box moves only the ein rows every tile owns)
-    mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
-    if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
-      tma_load_5d(stage_buf(s), &xmap, &bars[s], int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
-    else
-      tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
-    if (sb || TVSL) {
+    if (parts & 1) {
+      // (a masked box moves only the ein rows every tile owns)
+      mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
+      if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
+        tma_load_5d(stage_buf(s), &xmap, &bars[s], int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
+      else
+        tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
+    }
+    if ((parts & 6) && (sb || TVSL)) {
       // the tile's contiguous spectrum (or pre / post) and twiddle slices ride
       // on the same barrier
       const size_t g = size_t(tile_goff(t));
-      if (sb) {
+      if (sb && (parts & 2)) {
         const unsigned char* src =
             MID ? reinterpret_cast<const unsigned char*>(p.mid) + g * p.mid_gmul * sizeof(C)
                 : side_pre ? reinterpret_cast<const unsigned char*>(p.pre) + g * p.pre_gmul * sizeof(C)
                            : reinterpret_cast<const unsigned char*>(p.post) + g * p.post_gmul * sizeof(C);
         bulk_load(stage_spec(s), src, sb, &bars[s]);
       }
-      if constexpr (TVSL)
-        bulk_load(stage_tv(s), reinterpret_cast<const unsigned char*>(p.tw_slices) + g * N * 16, uint32_t(G::TVSB),
-                  &bars[s]);
+      if constexpr (TVSL) {
+        if (parts & 4)
+          bulk_load(stage_tv(s), reinterpret_cast<const unsigned char*>(p.tw_slices) + g * N * 16, uint32_t(G::TVSB),
+                    &bars[s]);
+      }
     }
   };
   // rows ein .. ein+npatch-1: thread tid < npatch*CT owns row ein + tid/CT,
@@ -462,7 +475,22 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       static_assert(CT == 32 || CT == 64, "the fused Kron Walsh-Hadamard needs 32- or 64-column tiles");
       if constexpr (!(FFT_SKIP & 4)) wht_lanes8<C, E, CT>(a);
     }
-    if constexpr (!(FFT_SKIP & 1)) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
+    // Early refill (direct-store masked complex128 passes with one landing
+    // buffer): once the last stage's inputs are in registers nothing reads
+    // the landing buffer again, so the next tile's box is issued there — its
+    // latency runs under the last radix-16 stage, the epilogue and the stores
+    // instead of after them.
+    auto early_refill = [&]() {
+      __syncthreads();
+      if (tid == 0 && t + G::NBUF * gs < ntiles) {
+        fence_proxy_async();
+        issue(t + G::NBUF * gs, sidx, 1 | (EARLY_SIDE && side_pre ? 2 : 0) | (EARLY_SIDE && twpre ? 4 : 0));
+      }
+    };
+    if constexpr (!(FFT_SKIP & 1)) {
+      if constexpr (EARLY) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, early_refill);
+      else fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
+    }
     if constexpr (MID) {
       constexpr int RF = st_radix(N, E, NST - 1, false);
       // the tile's spectrum slice landed in shared memory with the data
@@ -509,10 +537,11 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       if constexpr (!(FFT_SKIP & 1)) fft_stages<C, N, E, CT, true, 0, LAY, N, true, MID>(a, buf, j, cs, tws_mir);
     }
     // all exchange reads of the landing buffer are done after this barrier
-    __syncthreads();
+    // (the early refill's barrier already was that point)
+    if constexpr (!EARLY) __syncthreads();
     // (the epilogue still reads a post slice or output twiddle slice of the stage)
     const bool late_refill = side_post || (TVSL && !twpre);
-    if constexpr (!TS) {
+    if constexpr (!TS && !EARLY) {
       // the landing buffer is free: start the load NBUF tiles ahead (after the
       // epilogue when it still reads the stage's side area)
       if (!late_refill && tid == 0 && t + G::NBUF * gs < ntiles) {
@@ -608,7 +637,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         }
       }
     }
-    if constexpr (!TS) {
+    if constexpr (EARLY) {
+      __syncthreads();  // side area read
+      if (tid == 0 && t + G::NBUF * gs < ntiles) {
+        fence_proxy_async();
+        issue(t + G::NBUF * gs, sidx, (EARLY_SIDE && side_pre ? 0 : 2) | (EARLY_SIDE && twpre ? 0 : 4));
+      }
+    } else if constexpr (!TS) {
       if (TW || late_refill) __syncthreads();  // tile twiddles are rebuilt next / side area read
       if (late_refill && tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
@@ -729,7 +764,11 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
     return false;
   }
   // TMA-store epilogue when the output view is TMA-compatible as well
-  const bool ts = eout > 0 &&
+  // complex128 1024-point masked twiddle passes (one landing buffer, two CTAs
+  // per SM: the C5 outer passes) store per thread and refill the buffer early,
+  // except the pass whose fused Walsh-Hadamard runs on the staged output tile
+  const bool direct = sizeof(C) == 16 && NB == 1 && msk && a.tw_on && !a.mid && a.wht_half != 2 && !a.wht_grp && !blo;
+  const bool ts = eout > 0 && !direct &&
                   (a.wht_grp ? true
                              : make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
                                              blo ? blo : trunc ? rlo : 0, trunc ? eout : 0, trunc,
