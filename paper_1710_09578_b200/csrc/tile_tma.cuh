@@ -184,6 +184,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   C* tws = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE);  // W_N^t, t < N (float4 quads or double2)
   C* tvs = reinterpret_cast<C*>(smem_raw + G::NBUF * G::STAGE + G::TWB);  // four-step twiddles of the tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + G::NBUF * G::STAGE + G::TWB + G::TVB);
+  // (early-refill passes: the slice only the epilogue reads completes on its own barrier)
+  uint64_t* bars_e = bars + G::NBUF;
   const int tid = threadIdx.x, cs = tid % CT, j = tid / CT;
   const uint32_t f = p.flags;
   const R sx = ((f & F_CONJX) != 0) != (!MID && (f & F_INV)) ? R(-1) : R(1);
@@ -197,6 +199,9 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   const R smid = (f & F_MIDCONJ) ? R(-1) : R(1);
 
   const bool side_pre = MSK && (f & F_SIDEPRE) != 0, side_post = MSK && (f & F_SIDEPOST) != 0;
+  // early-refill passes: the slices read only by the epilogue (post vector,
+  // output twiddles) — issued after it, waited for right before the next one
+  const int emask = EARLY ? ((side_post ? 2 : 0) | (G::TVSL && !(TW && (f & F_TWPRE)) ? 4 : 0)) : 0;
   auto tile_goff = [&](int t) -> int {
     const uint32_t q = fdiv(uint32_t(t) * CT, p.gdiv.m, p.gdiv.s);
     return int(q - fdiv(q, p.gmod.m, p.gmod.s) * p.gmod.d);
@@ -209,14 +214,16 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     uint32_t o1, o2, c0;
     decode_batch(uint32_t(t) * CT, p.inner.d, p.inner.m, p.inner.s, p.n2.d, p.n2.m, p.n2.s, o1, o2, c0);
     const uint32_t sb = MID ? uint32_t(N * sizeof(C)) : (side_pre || side_post) ? uint32_t(N * sizeof(C)) : 0u;
+    const uint32_t eb = ((emask & 2) ? sb : 0u) + ((emask & 4) ? uint32_t(G::TVSB) : 0u);
     if (parts & 1) {
       // (a masked box moves only the ein rows every tile owns)
-      mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb);
+      mbar_arrive_expect_tx(&bars[s], uint32_t(ein * CT * int(sizeof(C)) + G::TVSB) + sb - eb);
       if (f & F_WGRP)  // (4 real columns x 8 hh: virtual column c0 -> real column c0 / 8)
         tma_load_5d(stage_buf(s), &xmap, &bars[s], int((c0 / 8) * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
       else
         tma_load_5d(stage_buf(s), &xmap, &bars[s], int(c0 * (sizeof(C) / 8)), 0, 0, int(o2), int(o1));
     }
+    if ((parts & emask) && eb) mbar_arrive_expect_tx(&bars_e[s], eb);  // (the epilogue's slices go out in one call)
     if ((parts & 6) && (sb || TVSL)) {
       // the tile's contiguous spectrum (or pre / post) and twiddle slices ride
       // on the same barrier
@@ -226,12 +233,12 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
             MID ? reinterpret_cast<const unsigned char*>(p.mid) + g * p.mid_gmul * sizeof(C)
                 : side_pre ? reinterpret_cast<const unsigned char*>(p.pre) + g * p.pre_gmul * sizeof(C)
                            : reinterpret_cast<const unsigned char*>(p.post) + g * p.post_gmul * sizeof(C);
-        bulk_load(stage_spec(s), src, sb, &bars[s]);
+        bulk_load(stage_spec(s), src, sb, (emask & 2) ? &bars_e[s] : &bars[s]);
       }
       if constexpr (TVSL) {
         if (parts & 4)
           bulk_load(stage_tv(s), reinterpret_cast<const unsigned char*>(p.tw_slices) + g * N * 16, uint32_t(G::TVSB),
-                    &bars[s]);
+                    (emask & 4) ? &bars_e[s] : &bars[s]);
       }
     }
   };
@@ -261,6 +268,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   if (tid == 0) {
     tma_prefetch_desc(&xmap);
     for (int s = 0; s < G::NBUF; ++s) mbar_init(&bars[s], 1);
+    if constexpr (EARLY)
+      for (int s = 0; s < G::NBUF; ++s) mbar_init(&bars_e[s], 1);
     fence_barrier_init();
     for (int s = 0; s < G::NBUF; ++s)
       if (int(blockIdx.x) + s * gs < ntiles) issue(blockIdx.x + s * gs, s);
@@ -484,7 +493,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       __syncthreads();
       if (tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
-        issue(t + G::NBUF * gs, sidx, 1 | (EARLY_SIDE && side_pre ? 2 : 0) | (EARLY_SIDE && twpre ? 4 : 0));
+        issue(t + G::NBUF * gs, sidx,
+              1 | (EARLY_SIDE && WH != 2 && side_pre ? 2 : 0) | (EARLY_SIDE && WH != 2 && twpre ? 4 : 0));
       }
     };
     if constexpr (!(FFT_SKIP & 1)) {
@@ -552,6 +562,10 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     // ---- epilogue: four-step twiddle, conj/scale, then either direct stores
     //      (TS = false) or a staged tile written back by one TMA store
     C* yc = (C*)p.y + yb;
+    if constexpr (EARLY) {
+      // (the epilogue's slices were issued after the previous tile's epilogue)
+      if (emask) mbar_wait(&bars_e[sidx], uint32_t((it / G::NBUF) & 1));
+    }
 #pragma unroll
     for (int u = 0; u < E / RL; ++u) {
       const int bb = j + u * TPC;
@@ -616,13 +630,34 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         }
       }
       if constexpr (WH == 2 && WHREG && !(FFT_SKIP & 2)) wht_regs_half(au);
+      if constexpr (WH == 2 && !TS) {
+        // Direct-store variant of the fused output Walsh-Hadamard: its
+        // shared-memory stages (strides < TPC over the first N/2 rows, 32 KB
+        // for a 4-column complex128 tile) run in the stage's side area, dead
+        // once the post multiply above has read it — the landing buffer is
+        // being refilled meanwhile — and the finished rows go straight to HBM.
+        static_assert(WHREG && E == RL && G::SPB + G::TVSB >= size_t(N / 2) * CT * sizeof(C),
+                      "the side area must hold the first half of the tile");
+        C* scr = reinterpret_cast<C*>(stage_spec(sidx));
+        __syncthreads();  // every thread has read its post / twiddle slice entries
 #pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const int k = bb + r * (N / RL);
-        if constexpr (TS) {
-          buf[k * CT + cs] = au[r];
-        } else if (!MSK || k < vout) {
-          yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+        for (int r = 0; r < 8; ++r) scr[(bb + r * TPC) * CT + cs] = au[r];
+        __syncthreads();
+        if constexpr (!(FFT_SKIP & 2)) tile_wht_half<C, N, CT, TPC, 1, TPC>(scr, j, cs);  // (ends with a barrier)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int k = bb + r * TPC;
+          if (k < vout) yk[int64_t(r * TPC) * p.ysi] = scr[k * CT + cs];
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int k = bb + r * (N / RL);
+          if constexpr (TS) {
+            buf[k * CT + cs] = au[r];
+          } else if (!MSK || k < vout) {
+            yk[int64_t(r * (N / RL)) * p.ysi] = au[r];
+          }
         }
       }
       if constexpr (MSK && TS) {
@@ -641,7 +676,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       __syncthreads();  // side area read
       if (tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
-        issue(t + G::NBUF * gs, sidx, (EARLY_SIDE && side_pre ? 0 : 2) | (EARLY_SIDE && twpre ? 0 : 4));
+        issue(t + G::NBUF * gs, sidx,
+              (EARLY_SIDE && WH != 2 && side_pre ? 0 : 2) | (EARLY_SIDE && WH != 2 && twpre ? 0 : 4));
       }
     } else if constexpr (!TS) {
       if (TW || late_refill) __syncthreads();  // tile twiddles are rebuilt next / side area read
@@ -767,7 +803,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   // complex128 1024-point masked twiddle passes (one landing buffer, two CTAs
   // per SM: the C5 outer passes) store per thread and refill the buffer early,
   // except the pass whose fused Walsh-Hadamard runs on the staged output tile
-  const bool direct = sizeof(C) == 16 && NB == 1 && msk && a.tw_on && !a.mid && a.wht_half != 2 && !a.wht_grp && !blo;
+  const bool direct = sizeof(C) == 16 && NB == 1 && msk && a.tw_on && !a.mid && !a.wht_grp && !blo;
   const bool ts = eout > 0 && !direct &&
                   (a.wht_grp ? true
                              : make_view_map(&ymap, a.y, sizeof(C), n1, a.ys1, a.n2, a.ys2, N, a.ysi, a.inner, G::CT,
@@ -827,7 +863,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
         // (the fused Walsh-Hadamard variants: complex128 passes of the C5 chain)
         if constexpr (sizeof(C) == 16 && N >= 256) {
           if (a.wht_half == 1) return pick(ts_tag, F_{}, T_{}, T_{}, std::integral_constant<int, 1>{});
-          if constexpr (decltype(ts_tag)::value) {
+          if constexpr (decltype(ts_tag)::value || (N == 1024 && NB == 1)) {
             if (a.wht_half == 2) return pick(ts_tag, F_{}, T_{}, T_{}, std::integral_constant<int, 2>{});
           }
         }
