@@ -174,6 +174,18 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   constexpr int R0 = st_radix(N, E, 0, false);
   constexpr int RL = MID ? st_radix(N, E, NST - 1, true) : st_radix(N, E, NST - 1, false);
   constexpr int LQ = log2_c(RL);
+  // Deferred refill (spectrum passes, ring of two or three buffers): the
+  // thread that issued a tile's TMA store does not wait for the engine to
+  // finish reading the buffer — its warp would start the next tile late and
+  // hold every barrier of it — but refills the buffer from inside the next
+  // tile's forward transform, before its last stage: the store has drained by
+  // then and the load still has the spectrum multiply and the inverse
+  // transform to land (C5 spectrum pass 2.64 -> 2.34 ms, C2 0.285 -> 0.269,
+  // C4 0.305 -> 0.274).  The passes with a single transform need the longer
+  // load lead (C2's twiddle / plain passes 0.207 / 0.183 -> 0.230 / 0.212 ms
+  // deferred) and keep the wait.
+  constexpr bool DEFER = TS && MID && G::NBUF >= 2 && NST >= 2 && !(FFT_SKIP & 1);
+  int pend_t = -1;
   constexpr bool EARLY = !TS && !MID && MSK && TW && sizeof(C) == 16 && G::NBUF == 1 && NST >= 2 && G::TVSL && !(FFT_SKIP & 1);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // stage s: [tile data | spectrum slice] at smem_raw + s*STAGE
@@ -497,8 +509,16 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
               1 | (EARLY_SIDE && WH != 2 && side_pre ? 2 : 0) | (EARLY_SIDE && WH != 2 && twpre ? 4 : 0));
       }
     };
+    auto deferred_refill = [&]() {
+      if (tid == 0 && pend_t >= 0) {
+        bulk_wait_read0();
+        issue(pend_t, (it + G::NBUF - 1) % G::NBUF);
+        pend_t = -1;
+      }
+    };
     if constexpr (!(FFT_SKIP & 1)) {
-      if constexpr (EARLY) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, early_refill);
+      if constexpr (DEFER) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, deferred_refill);
+      else if constexpr (EARLY) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, early_refill);
       else fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
     }
     if constexpr (MID) {
@@ -705,7 +725,9 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         // refill the buffer once the store has read it (deferring the refill
         // into the next tile removes this wait but shortens the load lead by
         // a tile, which measured slower)
-        if (t + G::NBUF * gs < ntiles) {
+        if constexpr (DEFER) {
+          pend_t = t + G::NBUF * gs < ntiles ? t + G::NBUF * gs : -1;
+        } else if (t + G::NBUF * gs < ntiles) {
           bulk_wait_read0();
           issue(t + G::NBUF * gs, sidx);
         }
