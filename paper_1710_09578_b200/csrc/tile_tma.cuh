@@ -95,7 +95,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // SMAX: the strides handled here (the stages with stride >= SMAX = TPC — the
 // bits of the stage-0 element index r — run in registers on the loaded /
 // finished elements instead, wht_regs_half).
-template <class C, int N, int CT, int TPC, int S = 1, int SMAX = N / 2>
+// SWZ: rows stored at row ^ ((row >> 3) & 1) — the stride-1 stage's threads
+// own 8 consecutive 64-byte rows each (512 bytes apart between lanes, all on
+// one half of the banks); flipping the low row bit of every other group puts
+// neighbouring lanes on opposite halves (a buffer the kernel fills itself).
+template <bool SWZ>
+__device__ __forceinline__ int wht_row(int row) {
+  return SWZ ? row ^ ((row >> 3) & 1) : row;
+}
+template <class C, int N, int CT, int TPC, int S = 1, int SMAX = N / 2, bool SWZ = false>
 __device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
   constexpr int NH = N / 2;
   static_assert(NH == 8 * TPC, "8 elements per thread");
@@ -107,13 +115,13 @@ __device__ __forceinline__ void tile_wht_half(C* buf, int j, int cs) {
       const int base = (gid / S) * (S * R) + gid % S;
       C v[8];
 #pragma unroll
-      for (int k = 0; k < R; ++k) v[k] = buf[(base + k * S) * CT + cs];
+      for (int k = 0; k < R; ++k) v[k] = buf[wht_row<SWZ>(base + k * S) * CT + cs];
       wht_small<R>(v);
 #pragma unroll
-      for (int k = 0; k < R; ++k) buf[(base + k * S) * CT + cs] = v[k];
+      for (int k = 0; k < R; ++k) buf[wht_row<SWZ>(base + k * S) * CT + cs] = v[k];
     }
     __syncthreads();
-    tile_wht_half<C, N, CT, TPC, S * R, SMAX>(buf, j, cs);
+    tile_wht_half<C, N, CT, TPC, S * R, SMAX, SWZ>(buf, j, cs);
   }
 }
 
@@ -661,13 +669,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         C* scr = reinterpret_cast<C*>(stage_spec(sidx));
         __syncthreads();  // every thread has read its post / twiddle slice entries
 #pragma unroll
-        for (int r = 0; r < 8; ++r) scr[(bb + r * TPC) * CT + cs] = au[r];
+        for (int r = 0; r < 8; ++r) scr[wht_row<true>(bb + r * TPC) * CT + cs] = au[r];
         __syncthreads();
-        if constexpr (!(FFT_SKIP & 2)) tile_wht_half<C, N, CT, TPC, 1, TPC>(scr, j, cs);  // (ends with a barrier)
+        if constexpr (!(FFT_SKIP & 2)) tile_wht_half<C, N, CT, TPC, 1, TPC, true>(scr, j, cs);  // (ends with a barrier)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int k = bb + r * TPC;
-          if (k < vout) yk[int64_t(r * TPC) * p.ysi] = scr[k * CT + cs];
+          if (k < vout) yk[int64_t(r * TPC) * p.ysi] = scr[wht_row<true>(k) * CT + cs];
         }
       } else {
 #pragma unroll
