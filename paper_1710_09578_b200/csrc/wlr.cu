@@ -83,6 +83,16 @@ constexpr int NSD = WLR_NSD;             // data ring stages
 #define WLR_NSF 2
 #endif
 constexpr int NSF = WLR_NSF;             // factor ring stages
+// tensor-phase step after which a warp hands the pipe over (contraction: of
+// 16 k-steps; expansion: of 4 row quarters, counted when quarter SIG_QR + 1's
+// products have been issued)
+#ifndef WLR_SIG_KS
+#define WLR_SIG_KS 12
+#endif
+#ifndef WLR_SIG_QR
+#define WLR_SIG_QR 2
+#endif
+constexpr int SIG_KS = WLR_SIG_KS, SIG_QR = WLR_SIG_QR;
 // (timing experiments only, tools/exp_build.py: skip phases; results wrong)
 #ifndef WLR_SKIP
 #define WLR_SKIP 0
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) {
     for (int st = 0; st < NSD; ++st) mbar_init(&full[st], 1);
     for (int st = 0; st < NSF; ++st) mbar_init(&ffull[st], 1);
-    for (int g = 0; g < NGRP; ++g) mbar_init(&mma_done[g], 1);
+    for (int g = 0; g < NGRP; ++g) mbar_init(&mma_done[g], GTHR / 32);  // (one arrival per warp)
     fence_barrier_init();
   }
   __syncthreads();
@@ -265,13 +275,20 @@ __global__ void __launch_bounds__(NTHR, 1)
       group_sync(grp);
     }
   };
-  auto mma_release = [&](int i) {
+  // Hand-over of the tensor pipe: every warp signals once most of its unit's
+  // MMAs are issued (SIG of the phase's steps), so the other group's waits,
+  // first operand loads and Gauss sums run under this group's last steps
+  // instead of after its release barrier; the release then only frees the
+  // factor stage.
+  auto mma_signal = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&mma_done[grp]);
+  };
+  auto mma_release = [&](int i, bool signalled) {
+    if (!signalled) mma_signal();
     fence_proxy_async();
     group_sync(grp);
-    if (gt == 0) {
-      mbar_arrive1(&mma_done[grp]);
-      if (i + NSF < nloc) issue_factor(i + NSF);  // (factor stage free)
-    }
+    if (gt == 0 && i + NSF < nloc) issue_factor(i + NSF);  // (factor stage free)
   };
   // contraction partials: q-tile mt (rows 8mt.. of W), product p (Gauss), pair
   double acc[4][3][2];
@@ -343,11 +360,12 @@ __global__ void __launch_bounds__(NTHR, 1)
           dmma(acc[mt][1], fc[mt].y, xc.y);
           dmma(acc[mt][2], fd[mt], bs);
         }
+        if (ks == SIG_KS) mma_signal();
       }
     }
     // (the release's group barrier also ends the contraction's reads of the
     // untransformed rows)
-    if constexpr (CON) mma_release(i);
+    if constexpr (CON) mma_release(i, !(WLR_SKIP & 1));
     if constexpr (NW > 1 && !(WLR_SKIP & 2)) {
       const int c = gt % KC, p = gt / KC;
       wht_stage<(NW < 8 ? NW : 8), 1, NW>(dbuf, c, p);  // strides 1, 2, 4
@@ -412,12 +430,13 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
       for (int qr = 0; qr < 4; ++qr) {
         if (qr + 1 < 4) mma_q(qr + 1, e[(qr + 1) & 1]);
-        else mma_release(i);
+        else mma_release(i, true);
+        if (qr == SIG_QR) mma_signal();
         rmw_q(qr, e[qr & 1]);
       }
       group_sync(grp);  // (the expanded rows are complete before the stores read them)
     } else if constexpr (EXP) {
-      mma_release(i);
+      mma_release(i, false);
     }
     if constexpr (OUT && !(WLR_SKIP & 8)) {
       // thread: column c, rows t = gt / 32 + 4 j (coalesced 512-byte rows)
