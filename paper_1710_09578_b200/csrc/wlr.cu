@@ -66,8 +66,11 @@ constexpr int FPE = (RK + 4) * 16;  // 576, expansion
 // units ahead of the consumers.  The groups' tensor-core phases (contraction
 // / expansion) are serialised in unit order through two mbarriers, so one
 // group multiplies while the other transforms and stores (left to themselves
-// the groups phase-lock: both multiply at half rate, then both stream); the
-// factor rows are needed only in that phase, hence their shorter ring.  Eight
+// the groups phase-lock: both multiply at half rate, then both stream); a
+// group hands the pipe over when three quarters of its unit's MMAs are issued
+// (one arrival per warp), so the other group's waits and first operand loads
+// run under its last steps.  The factor rows are needed only in that phase,
+// hence their shorter ring.  Eight
 // warps, two per SM sub-partition, leave each thread up to 255 registers
 // (a ninth, producer warp would cap them at 168 and spill the expansion).
 // (The single-stage two-CTA layout measured load + tensor work + transform +
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   // (the acquire also waits for the unit's factor rows and zeroes the rows
   // past the factor's end; the release frees their stage)
   auto mma_acquire = [&](int i, unsigned char* fbuf, int rf) {
-    if (i > 0) mbar_wait(&mma_done[1 - grp], uint32_t(((i - 1) / NGRP) & 1));
+    if (i > 0 && !(WLR_SKIP & 32)) mbar_wait(&mma_done[1 - grp], uint32_t(((i - 1) / NGRP) & 1));
     mbar_wait(&ffull[i % NSF], uint32_t((i / NSF) & 1));
     if (rf < TR) {
       for (int e = rf * (FP / 16) + gt; e < TR * (FP / 16); e += GTHR) st2(fbuf + e * 16, make_double2(0.0, 0.0));
@@ -341,10 +344,10 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int mt = 0; mt < 4; ++mt) fv[mt] = ld2(fr0 + mt * 128);
 #pragma unroll
       for (int ks = 0; ks < TR / 4; ++ks) {
-        const double bs = xv.x + xv.y;
+        const double bs = (WLR_SKIP & 64) ? xv.x : xv.x + xv.y;
         double fd[4];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) fd[mt] = fv[mt].x - fv[mt].y;
+        for (int mt = 0; mt < 4; ++mt) fd[mt] = (WLR_SKIP & 64) ? fv[mt].x : fv[mt].x - fv[mt].y;
         const double2 xc = xv;
         double2 fc[4];
 #pragma unroll
