@@ -388,6 +388,35 @@ def test_c5_blocked_chain(N, K):
     _close(op.backward(X), orc.apply(oo, X, 1), 1e-12, f"C5 blocked bwd N={N} K={K}")
 
 
+@pytest.mark.parametrize("K", [8, 12])
+def test_1024_point_outer_passes(K):
+    """Bluestein length 2^20 = 1024 x 1024: the complex128 1024-point masked
+    twiddle passes (per-thread stores, landing buffer refilled from inside the
+    transform, epilogue slice on its own barrier) at a second geometry than
+    C5's — plain Diag·Fourier·Diag (no fused Walsh-Hadamard, patch rows) and
+    the blocked chain (fused input / output Walsh-Hadamard, N1 = 16 x 64) —
+    plus the spectrum pass's deferred refill at 1024 points."""
+    N = 300_007
+    rng = np.random.default_rng(N + K)
+    d1 = np.exp(2j * np.pi * rng.random(N))
+    d2 = np.exp(2j * np.pi * rng.random(N))
+    X = (rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))) / np.sqrt(2)
+    op = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2))
+    ref = orc.product(orc.diagonal(d1), orc.fourier(N), orc.diagonal(d2))
+    _close(op.forward(X), orc.apply(ref, X, 0), 1e-12, f"DFD fwd N={N} K={K}")
+    _close(op.backward(X), orc.apply(ref, X, 1), 1e-12, f"DFD bwd N={N} K={K}")
+    U = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    V = (rng.standard_normal((N, 32)) + 1j * rng.standard_normal((N, 32))) / np.sqrt(2 * N)
+    idx = np.arange(N)
+    order = (N - 1).bit_length()
+    chain = sm.Product(sm.Diag(d1), sm.Fourier(N), sm.Diag(d2),
+                       sm.Sum(sm.Partial(sm.Hadamard(order), idx, idx), sm.LowRank(U, V)))
+    assert "BlockedChain" in chain.plan_for(np.complex128).describe()
+    oo = orc.chain_c5(N, d1, d2, U, V)
+    _close(chain.forward(X), orc.apply(oo, X, 0), 1e-12, f"chain fwd N={N} K={K}")
+    _close(chain.backward(X), orc.apply(oo, X, 1), 1e-12, f"chain bwd N={N} K={K}")
+
+
 @pytest.mark.parametrize("order,K", [(6, 1), (10, 3), (13, 2), (21, 1)])
 def test_partial_hadamard_fused_selection(order, K):
     """Partial(Hadamard) with unique arbitrary row / column selections runs as
