@@ -190,9 +190,13 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   // then and the load still has the spectrum multiply and the inverse
   // transform to land (C5 spectrum pass 2.64 -> 2.34 ms, C2 0.285 -> 0.269,
   // C4 0.305 -> 0.274).  The passes with a single transform need the longer
-  // load lead (C2's twiddle / plain passes 0.207 / 0.183 -> 0.230 / 0.212 ms
-  // deferred) and keep the wait.
-  constexpr bool DEFER = TS && MID && G::NBUF >= 2 && NST >= 2 && !(FFT_SKIP & 1);
+  // load lead (C2's 1024-point twiddle / plain passes 0.207 / 0.183 -> 0.230 /
+  // 0.212 ms deferred) and keep the wait.
+  // Short transforms (<= 256 points: C4's and C3's passes, 64 KB tiles of
+  // many columns) defer in every pass, at the start of the transform (C4
+  // 0.886 -> 0.877 ms per step, C3 0.305 -> 0.302).
+  constexpr bool DEFER = TS && (MID || N <= 256) && G::NBUF >= 2 && NST >= 2 && !(FFT_SKIP & 1);
+  constexpr bool DEFER_START = DEFER && N <= 256;
   int pend_t = -1;
   constexpr bool EARLY = !TS && !MID && MSK && TW && sizeof(C) == 16 && G::NBUF == 1 && NST >= 2 && G::TVSL && !(FFT_SKIP & 1);
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -525,7 +529,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       }
     };
     if constexpr (!(FFT_SKIP & 1)) {
-      if constexpr (DEFER) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, deferred_refill);
+      if constexpr (DEFER_START) deferred_refill();
+      if constexpr (DEFER && !DEFER_START) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, deferred_refill);
       else if constexpr (EARLY) fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws, early_refill);
       else fft_stages<C, N, E, CT, false, 0, LAY, N, true, MID>(a, buf, j, cs, tws);
     }
