@@ -55,7 +55,10 @@ struct TmaGeom {
   // list is a palindrome (the mirrored inverse of the spectrum pass shares it),
   // else a second one for the mirrored list (short transforms only)
   static constexpr bool DUAL = !st_palindrome(N, E);
-  static constexpr size_t TWB = size_t(N) * 16 * (DUAL ? 2 : 1);
+  // (entries: float4 quads / double2, or plain float2 in the single-precision
+  // spectrum passes — 8 KB less there lets C2's spectrum pass run a three-deep ring)
+  static constexpr size_t TWE = (MS == 1 && sizeof(C) == 8) ? 8 : 16;
+  static constexpr size_t TWB = size_t(N) * TWE * (DUAL ? 2 : 1);
   static constexpr size_t TVB = TV && !TVSL ? size_t(N) * 16 : 0;  // per-tile four-step twiddles
   // ring of landing buffers: tile t computes in one while t+1.. load into the others
   static constexpr int NBUF =
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
   // when it is a palindrome and shares the table, else reads a second one
   constexpr bool DUAL = MID && G::DUAL;
   // (16-byte entries: float4 quads or double2)
-  C* tws_mir = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(tws) + (DUAL ? N * 16 : 0));
+  C* tws_mir = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(tws) + (DUAL ? N * int(G::TWE) : 0));
 #pragma unroll
   for (int half = 0; half < (DUAL ? 2 : 1); ++half) {
     const bool mir = half == 1;
