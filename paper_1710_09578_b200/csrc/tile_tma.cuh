@@ -56,7 +56,7 @@ struct TmaGeom {
   // else a second one for the mirrored list (short transforms only)
   static constexpr bool DUAL = !st_palindrome(N, E);
   // (entries: float4 quads / double2, or plain float2 in the single-precision
-  // spectrum passes — 8 KB less there lets C2's spectrum pass run a three-deep ring)
+  // spectrum passes)
   static constexpr size_t TWE = (MS == 1 && sizeof(C) == 8) ? 8 : 16;
   static constexpr size_t TWB = size_t(N) * TWE * (DUAL ? 2 : 1);
   static constexpr size_t TVB = TV && !TVSL ? size_t(N) * 16 : 0;  // per-tile four-step twiddles
@@ -80,10 +80,6 @@ struct TmaGeom {
 // (timing experiments only, tools/exp_build.py: skip phases; results wrong)
 #ifndef FFT_SKIP
 #define FFT_SKIP 0
-#endif
-
-#ifndef EARLY_SIDE
-#define EARLY_SIDE 1
 #endif
 
 template <class C, int N>
@@ -515,13 +511,14 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
     // buffer): once the last stage's inputs are in registers nothing reads
     // the landing buffer again, so the next tile's box is issued there — its
     // latency runs under the last radix-16 stage, the epilogue and the stores
-    // instead of after them.
+    // instead of after them — together with the slice the prologue reads (the
+    // fused output Walsh-Hadamard keeps the whole side area for its rows, WH = 2).
     auto early_refill = [&]() {
       __syncthreads();
       if (tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
         issue(t + G::NBUF * gs, sidx,
-              1 | (EARLY_SIDE && WH != 2 && side_pre ? 2 : 0) | (EARLY_SIDE && WH != 2 && twpre ? 4 : 0));
+              1 | (WH != 2 && side_pre ? 2 : 0) | (WH != 2 && twpre ? 4 : 0));
       }
     };
     auto deferred_refill = [&]() {
@@ -713,7 +710,7 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
       if (tid == 0 && t + G::NBUF * gs < ntiles) {
         fence_proxy_async();
         issue(t + G::NBUF * gs, sidx,
-              (EARLY_SIDE && WH != 2 && side_pre ? 0 : 2) | (EARLY_SIDE && WH != 2 && twpre ? 0 : 4));
+              (WH != 2 && side_pre ? 0 : 2) | (WH != 2 && twpre ? 0 : 4));
       }
     } else if constexpr (!TS) {
       if (TW || late_refill) __syncthreads();  // tile twiddles are rebuilt next / side area read
@@ -738,9 +735,8 @@ __global__ void __launch_bounds__(TmaGeom<C, N, EP, NB, TW, MID ? 1 : MSK ? 2 : 
         else
           tma_store_5d(&ymap, buf, int(c0 * (sizeof(C) / 8)), 0, 0, int(q2), int(q1));
         bulk_commit();
-        // refill the buffer once the store has read it (deferring the refill
-        // into the next tile removes this wait but shortens the load lead by
-        // a tile, which measured slower)
+        // refill the buffer once the store has read it — here, or (DEFER) from
+        // inside the next tile, where this thread no longer has to wait
         if constexpr (DEFER) {
           pend_t = t + G::NBUF * gs < ntiles ? t + G::NBUF * gs : -1;
         } else if (t + G::NBUF * gs < ntiles) {
@@ -839,8 +835,7 @@ inline bool fft_tma_launch_v(const FftArgs& a, cudaStream_t s) {
   }
   // TMA-store epilogue when the output view is TMA-compatible as well
   // complex128 1024-point masked twiddle passes (one landing buffer, two CTAs
-  // per SM: the C5 outer passes) store per thread and refill the buffer early,
-  // except the pass whose fused Walsh-Hadamard runs on the staged output tile
+  // per SM: the C5 outer passes) store per thread and refill the buffer early
   const bool direct = sizeof(C) == 16 && NB == 1 && msk && a.tw_on && !a.mid && !a.wht_grp && !blo;
   const bool ts = eout > 0 && !direct &&
                   (a.wht_grp ? true
