@@ -620,9 +620,11 @@ def run_native(args, cfg):
     value = 2 * K / (ms_step / 1e3)
 
     # per-launch profile and rooflines (eager, events on the launching stream)
-    fp_peaks = probe_peaks(dev) if rank == 0 else None
-    reps = 3
+    # (before the FP64 / FP32 peak probes: their power draw would carry into
+    # the FP64-heavy passes profiled right after them)
+    reps = 5
     plan, by = kernel_profile(cfg, op, X, dev, Kl, reps)
+    fp_peaks = probe_peaks(dev) if rank == 0 else None
     rf, passes = roofline_of(cfg, args.workload, by, Kl, ms_step * 1.0, reps, peak, peak_src, fp_peaks)
     launches = plan.launches(0, Kl) + plan.launches(1, Kl)
 
