@@ -635,8 +635,8 @@ def run_native(args, cfg):
         # block: the host path stages it with pitched copies (ABI ldx), no
         # host-side repacking inside or outside the timed region
         Xh = torch.from_numpy(np.ascontiguousarray(w.X)).pin_memory()[:, a:b]
-        e_steps = 3
-        for _ in range(2):  # the pinned caching allocator holds the blocks the loop cycles through
+        e_steps = max(3, min(int(args.steps), 10))
+        for _ in range(3):  # the pinned caching allocator holds the blocks the loop cycles through
             yh = op.forward(Xh)
             zh = op.backward(yh)
         torch.cuda.synchronize()
